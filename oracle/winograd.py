@@ -1,0 +1,130 @@
+"""oracle.winograd -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+The N-dimensional fast convolution of PAPER.md Sec. 3.2-3.3 and 4.1, step by
+step, over exact ``Fraction`` (object arrays) or float64:
+
+1. tiling into overlapping D^N tiles stepping by S (
+   DESIGN.md readings #2, #10: symmetric zero padding P, out = in + 2P - G + 1,
+   ceil(out/S) tiles per axis, tile t reads input [tS - P, tS - P + D)
+   zero-filled, outputs past `out` discarded);
+2. kernel transform  G x_{n=1}^N C_n   (Eq. (4)),
+   data transform    D x_{n=1}^N B_n,
+   each a chain of n-mode products (Eq. (3));
+3. per transform point i: S_hat^(i) = D_hat^(i) x G_hat^(i) with D_hat T x M
+   (tiles-by-channels) and G_hat M x K (Eq. (5)) -- the
+   element-wise product fused with the channel reduction;
+4. inverse transform  x_{n=1}^N A_n  and stitching.
+
+Matrices use the paper's orientation: A (S x D), B (D x D), C (D x G).
+No blocking, fusion or reordering beyond what Eq. (3)-(5) state.
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+import numpy as np
+
+
+def as_array(Mx, exact: bool):
+    if exact:
+        return np.array([[Fraction(v) for v in row] for row in Mx], dtype=object)
+    return np.array([[float(v) for v in row] for row in Mx], dtype=np.float64)
+
+
+def nmode_product(X: np.ndarray, U: np.ndarray, n: int) -> np.ndarray:
+    """(X x_n U)_{i1..j..iN} = sum_{i_n} x_{i1..i_n..iN} u_{j,i_n}  (Eq. (3))."""
+    Y = np.tensordot(U, X, axes=([1], [n]))     # new axis j first
+    return np.moveaxis(Y, 0, n)
+
+
+def multi_mode_product(X: np.ndarray, U: np.ndarray, axes) -> np.ndarray:
+    """X x_{n} U over the listed axes, left to right."""
+    for ax in axes:
+        X = nmode_product(X, U, ax)
+    return X
+
+
+def tile_geometry(in_dims, r: int, m: int, pad):
+    """out dims, tiles per axis, T per sample (readings #2, #10)."""
+    out = tuple(int(i) + 2 * int(p) - r + 1 for i, p in zip(in_dims, pad))
+    tiles = tuple(math.ceil(o / m) for o in out)
+    return out, tiles
+
+
+def extract_tiles(x: np.ndarray, m: int, alpha: int, pad, zero):
+    """x [B][C][in...] -> tiles [B][C][t_1..t_N][alpha]*N, zero-filled."""
+    N = x.ndim - 2
+    B, C = x.shape[:2]
+    r = alpha - m + 1
+    out, tiles = tile_geometry(x.shape[2:], r, m, pad)
+    res = np.empty((B, C) + tiles + (alpha,) * N, dtype=x.dtype)
+    res[...] = zero
+    for tidx in np.ndindex(*tiles):
+        for w in np.ndindex(*((alpha,) * N)):
+            src = tuple(tidx[n] * m - pad[n] + w[n] for n in range(N))
+            if all(0 <= src[n] < x.shape[2 + n] for n in range(N)):
+                res[(slice(None), slice(None)) + tidx + w] = x[(slice(None), slice(None)) + src]
+    return res, out, tiles
+
+
+def winograd_nd(x, g, pad, A, B, C, exact: bool = False):
+    """Full N-D Winograd layer.  Returns (y, stages) where stages holds
+    U [alpha^N][M][K] (G_hat^(i)), V [alpha^N][T][M] (D_hat^(i)),
+    Shat [alpha^N][T][K] (S_hat^(i)), with i row-major over the D^N
+    transform-domain coordinates and t row-major over (b, t_1..t_N)."""
+    A_ = as_array(A, exact)
+    B_ = as_array(B, exact)
+    C_ = as_array(C, exact)
+    S, D = A_.shape
+    Gk = C_.shape[1]
+    if exact:
+        x = np.asarray(x, dtype=object)
+        g = np.asarray(g, dtype=object)
+        zero = Fraction(0)
+    else:
+        x = np.asarray(x, dtype=np.float64)
+        g = np.asarray(g, dtype=np.float64)
+        zero = 0.0
+    N = x.ndim - 2
+    if np.isscalar(pad):
+        pad = (int(pad),) * N
+    Bn, M = x.shape[:2]
+    K = g.shape[0]
+    assert g.shape[2:] == (Gk,) * N
+
+    # (2) kernel transform: G x_{n=1}^N C  -> [K][M][D..D]
+    Ug = multi_mode_product(g, C_, range(2, 2 + N))
+    # (1)+(2) tiles and data transform: D x_{n=1}^N B
+    tiles, out, tgrid = extract_tiles(x, S, D, pad, zero)
+    Vt = multi_mode_product(tiles, B_, range(2 + N, 2 + 2 * N))   # [B][M][tiles][D..]
+    T = Bn * int(np.prod(tgrid))
+    P = D ** N
+    # i-major matrices of Eq. (5)
+    Ghat = Ug.reshape(K, M, P).transpose(2, 1, 0)                     # [P][M][K]
+    Dhat = np.moveaxis(Vt, 1, -1 - N)                                 # [B][tiles][M][D..]
+    Dhat = Dhat.reshape(T, M, P).transpose(2, 0, 1)                   # [P][T][M]
+    # (3) per transform point: S_hat^(i) = D_hat^(i) G_hat^(i)
+    Shat = np.empty((P, T, K), dtype=Dhat.dtype)
+    for i in range(P):
+        Shat[i] = np.dot(Dhat[i], Ghat[i])
+    # (4) inverse transform per (t, k) and stitch
+    St = Shat.transpose(1, 2, 0).reshape((T, K) + (D,) * N)
+    Yt = multi_mode_product(St, A_, range(2, 2 + N))                  # [T][K][S..S]
+    Yt = Yt.reshape((Bn,) + tgrid + (K,) + (S,) * N)
+    y = np.empty((Bn, K) + out, dtype=Dhat.dtype)
+    for b in range(Bn):
+        for tidx in np.ndindex(*tgrid):
+            for o in np.ndindex(*((S,) * N)):
+                dst = tuple(tidx[n] * S + o[n] for n in range(N))
+                if all(dst[n] < out[n] for n in range(N)):
+                    y[(b, slice(None)) + dst] = Yt[(b,) + tidx + (slice(None),) + o]
+    return y, {"U": Ghat, "V": Dhat, "Shat": Shat, "out": out, "tiles": tgrid}
+
+
+def winograd_2d_closed_form(d_tile, g_ker, A, B, C, exact: bool = False):
+    """The 2-D special case S = A[(C G C^T) (.) (B D B^T)] A^T."""
+    A_, B_, C_ = as_array(A, exact), as_array(B, exact), as_array(C, exact)
+    dt = np.asarray(d_tile, dtype=object if exact else np.float64)
+    gk = np.asarray(g_ker, dtype=object if exact else np.float64)
+    return A_.dot((C_.dot(gk).dot(C_.T)) * (B_.dot(dt).dot(B_.T))).dot(A_.T)
