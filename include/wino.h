@@ -1,0 +1,176 @@
+/*
+ * wino.h -- C ABI of libwino.so, the B200 (sm_100a) N-dimensional Winograd
+ * convolution layer F(m^N, r^N) of Budden et al., "Deep Tensor Convolution on
+ * Multicores" (arXiv 1611.06565).  Citations: PAPER.md:<line> of the paper
+ * text; DESIGN.md "readings" for every place the paper is silent.
+ *
+ * What one layer computes (Eq. (2), with b = 0, f = id):
+ *
+ *   y[b,k,o] = sum_c sum_{p in [0,r)^N} g[k,c,p] * xt[b,c,o+p-P]
+ *
+ * cross-correlation (no flip, reading #1), stride 1, symmetric zero padding P
+ * per axis (reading #2), out_n = in_n + 2 P_n - r + 1.  It is evaluated by the
+ * N-D fast algorithm of Eq. (4), batched per transform
+ * point as in Eq. (5):
+ *
+ *   a0 host: exact-rational Toom-Cook synthesis of A^T (m x alpha),
+ *      G (alpha x r), B^T (alpha x alpha), alpha = m + r - 1, from alpha
+ *      interpolation points          [plan_create]
+ *   a1 U_xi = (g[k,c] x_1 G ... x_N G)_xi   (kernel transform)  [filter_transform]
+ *   a2 V_xi = (tile(b,c,t) x_1 B^T ... x_N B^T)_xi  (data transform)   [forward]
+ *   a3 M_xi = V_xi U_xi, a [tiles x C] x [C x K] GEMM per point xi     [forward]
+ *   a4 y tile = M[.][k][t] x_1 A^T ... x_N A^T, cropped/scattered      [forward]
+ *
+ * Conventions for every call:
+ *  - Tensor pointers are DEVICE pointers (fp32, contiguous, row-major, on the
+ *    plan's device) unless the name says _host.  The caller owns x, g, y and
+ *    must keep them alive until the stream work completes.
+ *  - Layouts: x [B][C][in_1]..[in_N], g [K][C][r]..[r] (r^N), y [B][K][out_1]..[out_N]
+ *    (torch's contiguous convNd layout; reading #11).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls are stream-ordered and do not synchronise the host unless noted.
+ *  - No exception crosses the ABI.  On failure a call returns a nonzero
+ *    wino_status and wino_last_error() returns a thread-local message.
+ *  - Concurrency: one call at a time per plan; distinct plans
+ *    are independent.
+ */
+#ifndef WINO_H_
+#define WINO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define WINO_API __attribute__((visibility("default")))
+#else
+#define WINO_API
+#endif
+
+typedef struct wino_plan_s* wino_plan_t;
+typedef void* wino_stream_t; /* a cudaStream_t */
+
+typedef enum {
+  WINO_OK = 0,
+  WINO_ERR_ARG = 1,         /* N not in 1..4, m/r/C/K/batch < 1, NULL pointer, B > planned batch */
+  WINO_ERR_SHAPE = 2,       /* kernel larger than the padded input (out_n < 1) */
+  WINO_ERR_POINTS = 3,      /* point list unparsable, duplicate, >1 infinity, count != alpha */
+  WINO_ERR_SYNTH = 4,       /* exact identity check failed, or rational overflow */
+  WINO_ERR_STATE = 5,       /* forward before the filter transform */
+  WINO_ERR_UNSUPPORTED = 6, /* alpha or (alpha, N) not instantiated on the device path */
+  WINO_ERR_CUDA = 7,        /* CUDA launch/runtime error (incl. async errors surfaced here) */
+  WINO_ERR_NOMEM = 8        /* device or pinned allocation failed */
+} wino_status;
+
+/* GEMM schemes for stage a3 (all fp32-accurate except WINO_GEMM_1XTF32). */
+enum {
+  WINO_GEMM_AUTO = 0,   /* = WINO_GEMM_3XTF32 */
+  WINO_GEMM_FFMA = 1,   /* CUDA-core fp32 FMA, smem-tiled */
+  WINO_GEMM_1XTF32 = 2, /* single tf32 product: debug/accuracy experiments only */
+  WINO_GEMM_3XTF32 = 3  /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, TMEM fp32 accumulators */
+};
+
+/* Fusion bitmask (plan_create_ex `fuse`). */
+enum {
+  WINO_FUSE_NONE = 0,
+  WINO_FUSE_L2_CHUNK = 4 /* run a2->a3->a4 over tile chunks sized to stay L2-resident */
+};
+
+/* ---- plan lifetime -------------------------------------------------------
+ * wino_plan_create: validate arguments, synthesise the transforms exactly for
+ * the default points of alpha (reading #5), check the Eq. (1)
+ * identity exactly (else WINO_ERR_SYNTH), upload fp32/fp64 constants, and
+ * allocate the transformed-filter buffer U and the workspace (V, M) for up
+ * to `batch` samples on the current device.  No kernel is launched.
+ *   N        number of spatial dims, 1..4
+ *   dims     N input extents in_n >= 1
+ *   m, r     output-tile length S and kernel length G of F(m, r)
+ *   C, K     input channels M and output channels / kernels K
+ *   batch    largest batch a forward call will pass
+ *   padding  N symmetric zero-pad amounts P_n >= 0 (NULL = all zero)
+ * On success *plan owns all device memory it allocated. */
+WINO_API wino_status wino_plan_create(wino_plan_t* plan, int N, const int64_t* dims, int m, int r,
+                             int C, int K, int batch, const int* padding);
+
+/* As above with explicit choices.
+ *   points    NULL = default; else alpha comma-separated rationals in row
+ *             order, e.g. "0,3/2,-3/2,2/3,-2/3,inf" (at most one "inf").
+ *   gemm_mode WINO_GEMM_* (0 = 3xTF32 on tcgen05).
+ *   fuse      WINO_FUSE_* bitmask (0 = three stream-ordered kernels).
+ *   device    CUDA device ordinal, -1 = current. */
+WINO_API wino_status wino_plan_create_ex(wino_plan_t* plan, int N, const int64_t* dims, int m, int r,
+                                int C, int K, int batch, const int* padding, const char* points,
+                                int gemm_mode, int fuse, int device);
+
+/* Frees every device/host buffer of the plan.  The caller must ensure no work
+ * using the plan is still in flight (synchronise first).  NULL is a no-op. */
+WINO_API wino_status wino_plan_destroy(wino_plan_t plan);
+
+/* ---- hot path --------------------------------------------------------------
+ * a1: U = g x_n G (fp64 arithmetic, one rounding to fp32, then the tf32 hi/lo
+ * split), cached in the plan until the next call ("transformed kernels are
+ * cached").  g: device [K][C][r^N]. */
+WINO_API wino_status wino_filter_transform(wino_plan_t plan, const float* g, wino_stream_t stream);
+
+/* a2 -> a3 -> a4 on `stream`, no host synchronisation.  x: device
+ * [B][C][in...], y: device [B][K][out...], 1 <= B <= planned batch.
+ * WINO_ERR_STATE if no filter transform (or mark_ready) happened. */
+WINO_API wino_status wino_forward(wino_plan_t plan, const float* x, float* y, int B, wino_stream_t stream);
+
+/* End-to-end variant with HOST buffers: copies x_host (B x C x in...) to a
+ * plan-owned device buffer, runs wino_forward, copies y back to y_host and
+ * synchronises `stream` before returning.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for full PCIe bandwidth. */
+WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, float* y_host, int B,
+                              wino_stream_t stream);
+
+/* ---- queries ---------------------------------------------------------------- */
+/* out[0..N): output extents. */
+WINO_API wino_status wino_plan_out_dims(wino_plan_t plan, int64_t* out);
+/* Device bytes: workspace (V + M) and filter buffer (U_hi + U_lo). */
+WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, size_t* filter_bytes);
+/* info[0..16): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
+ * (alpha^N), K_stride, gemm_mode, fuse, n_blk, k_chunk, specialised(0/1). */
+WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
+
+/* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------
+ * The filter buffer (U_hi then U_lo, contiguous) for an external broadcast;
+ * after filling it on another rank call wino_filter_mark_ready. */
+WINO_API wino_status wino_filter_buffer(wino_plan_t plan, void** dev_ptr, size_t* bytes);
+WINO_API wino_status wino_filter_mark_ready(wino_plan_t plan);
+
+/* ---- test / stage hooks --------------------------------------------------------
+ * Device pointers of the unfused workspace: V [n_points][C][T_stride] and
+ * M [n_points][K][T_stride] (valid after a forward with fuse == 0). */
+WINO_API wino_status wino_workspace(wino_plan_t plan, void** V, void** M);
+
+/* Per-stage CUDA-event timing of forward calls (bench instrumentation).
+ * enable=1 starts recording (resets accumulators); ms[0..3) receives the
+ * summed milliseconds of input transform, GEMM, output transform over the
+ * recorded calls and *calls their number (synchronises the recorded events). */
+WINO_API wino_status wino_profile_enable(wino_plan_t plan, int enable);
+WINO_API wino_status wino_profile_read(wino_plan_t plan, double* ms, int* calls);
+
+/* Host-only exact synthesis (no device needed).  Fills, for F(m, r) with the
+ * given points (NULL = default), AT (m x alpha), G (alpha x r), BT
+ * (alpha x alpha) as doubles (RNE from exact rationals) and, if json != NULL,
+ * a JSON document {"m","r","alpha","points","AT","G","BT"} of exact rational
+ * strings (truncated to `cap` bytes, NUL-terminated). */
+WINO_API wino_status wino_synthesize(int m, int r, const char* points, double* AT, double* G, double* BT,
+                            char* json, size_t cap);
+/* The plan's transforms, same format. */
+WINO_API wino_status wino_get_transforms(wino_plan_t plan, double* AT, double* G, double* BT, char* json,
+                                size_t cap);
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+WINO_API const char* wino_last_error(void);
+/* Library version string. */
+WINO_API const char* wino_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINO_H_ */

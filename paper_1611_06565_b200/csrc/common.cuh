@@ -1,0 +1,83 @@
+// common.cuh -- shared device/host definitions of the B200 Winograd path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+#include <utility>
+
+#include "synth.hpp"
+
+namespace wino {
+
+constexpr int kMaxN = 4;      // spatial dims supported on the device path
+constexpr int kMaxA = 8;      // alpha <= 8 on the device path
+
+constexpr int ipow(int b, int e) { return e <= 0 ? 1 : b * ipow(b, e - 1); }
+
+// Compile-time loop: f(std::integral_constant<int, i>) for i in [B, E).
+template <int B, int E, class F>
+__host__ __device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    sfor<B + 1, E>(std::forward<F>(f));
+  }
+}
+
+// Geometry of one plan, passed by value (__grid_constant__) to the transform kernels.
+struct KGeom {
+  int64_t in[kMaxN];         // input extents
+  int64_t in_stride[kMaxN];  // element strides inside one (b, c) plane
+  int64_t out[kMaxN];        // output extents
+  int64_t out_stride[kMaxN];
+  int tiles[kMaxN];          // ceil(out / m)
+  int pad[kMaxN];
+  int64_t in_vol, out_vol;   // per (b, c) / (b, k) plane
+  int64_t Tps;               // tiles per sample
+  int64_t T;                 // tiles of this call (B * Tps)
+  int64_t T_s;               // row stride of V and M (>= planned T, multiple of 32)
+  int C, K;
+  int m;                     // output tile length (runtime copy)
+};
+
+// Runtime transform tables (generic path); constant-bank resident.
+struct XfParams {
+  float AT[kMaxA][kMaxA];
+  float BT[kMaxA][kMaxA];
+};
+
+// Tables for the filter transform (fp64).
+struct FParams {
+  double G[kMaxA][kMaxA];
+  int N, a, r, C, K, K_s;
+  int64_t P;  // a^N
+};
+
+// Table providers.  ConstTab<M, R, PS>: tables synthesised at compile time
+// into a __device__ constexpr object; inside fully unrolled loops every read
+// is a constant, so zero entries vanish and +-1 become FADDs.  RunTab: the
+// values come from XfParams at run time (any interpolation points).
+template <int M, int R, int PS>
+__device__ constexpr FloatTables kDevTab = to_tables(synthesize_default(M, R, PS));
+
+template <int M_, int R_, int PS_>
+struct ConstTab {
+  static constexpr bool kConst = true;
+  static_assert(synthesize_default(M_, R_, PS_).err == 0, "default synthesis failed");
+  __device__ static __forceinline__ float bt(const XfParams&, int x, int i) { return kDevTab<M_, R_, PS_>.BT[x][i]; }
+  __device__ static __forceinline__ float at(const XfParams&, int x, int i) { return kDevTab<M_, R_, PS_>.AT[x][i]; }
+};
+struct RunTab {
+  static constexpr bool kConst = false;
+  __device__ static __forceinline__ float bt(const XfParams& p, int x, int i) { return p.BT[x][i]; }
+  __device__ static __forceinline__ float at(const XfParams& p, int x, int i) { return p.AT[x][i]; }
+};
+
+// tf32 round-to-nearest (ties away) of an fp32 value, result as fp32 container.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+}  // namespace wino

@@ -1,0 +1,38 @@
+// kernels.h -- internal launchers (host side) of the device stages.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace wino {
+
+enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
+
+bool xform_supported(int N, int alpha, int m, int spec);
+cudaError_t launch_xform(bool input, int N, int alpha, int m, int spec, const float* src, float* dst,
+                         const KGeom& g, const XfParams& xp, cudaStream_t s);
+cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
+                                cudaStream_t s);
+
+// a3, CUDA-core fp32 FMA: Mo[xi][k][t] = sum_c V[xi][c][t] U[xi][c][k]
+cudaError_t launch_gemm_ffma(const float* V, const float* U32, float* Mo, int P, int64_t T, int64_t T_s,
+                             int C, int K, int K_s, cudaStream_t s);
+
+// a3 on tcgen05 tensor cores.
+struct TcGemm {
+  CUtensorMap tmA;    // V   [P][C][T_s]   (3-D map: t, c, xi)
+  CUtensorMap tmBhi;  // U_hi [P][C][K_s]
+  CUtensorMap tmBlo;  // U_lo
+  int bn;             // N tile (32, 64, 128, 256)
+  int kc;             // channels per pipeline stage (multiple of 8, <= 32)
+  int three;          // 1: 3xTF32, 0: 1xTF32
+  int num_sms;
+  bool ready;
+};
+cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,
+                            int64_t T_s, int C, int K_s, int K, int three, int device);
+cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K,
+                           cudaStream_t s);
+
+}  // namespace wino

@@ -1,0 +1,499 @@
+// plan.cu -- the C ABI of include/wino.h: argument validation, geometry,
+// exact transform synthesis (stage a0), device buffers, stage launches.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "synth.hpp"
+#include "wino.h"
+
+using namespace wino;
+
+namespace {
+
+thread_local std::string g_err;
+
+wino_status fail(wino_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? WINO_ERR_NOMEM : WINO_ERR_CUDA,       \
+                  "%s failed: %s", #expr, cudaGetErrorString(e_));                       \
+  } while (0)
+
+// ---- exact points --------------------------------------------------------
+bool parse_int(const char*& s, int64_t& v) {
+  while (*s == ' ') ++s;
+  bool neg = false;
+  if (*s == '+' || *s == '-') neg = (*s++ == '-');
+  if (*s < '0' || *s > '9') return false;
+  __int128 acc = 0;
+  while (*s >= '0' && *s <= '9') {
+    acc = acc * 10 + (*s++ - '0');
+    if (acc > (__int128)INT64_MAX) return false;
+  }
+  v = (int64_t)(neg ? -acc : acc);
+  return true;
+}
+
+// "0,3/2,-3/2,inf" -> points; returns count or -1
+int parse_points(const char* spec, Point* out, int cap) {
+  int n = 0;
+  const char* s = spec;
+  while (true) {
+    while (*s == ' ') ++s;
+    if (n >= cap) return -1;
+    Point p;
+    if (!strncmp(s, "inf", 3) || !strncmp(s, "INF", 3)) {
+      p.inf = true;
+      s += 3;
+      if (!strncmp(s, "inity", 5)) s += 5;
+    } else {
+      int64_t num, den = 1;
+      if (!parse_int(s, num)) return -1;
+      while (*s == ' ') ++s;
+      if (*s == '/') {
+        ++s;
+        if (!parse_int(s, den) || den == 0) return -1;
+      }
+      RatOps o;
+      p.v = o.make(num, den);
+      if (o.overflow) return -1;
+    }
+    out[n++] = p;
+    while (*s == ' ') ++s;
+    if (*s == ',') { ++s; continue; }
+    if (*s == 0) break;
+    return -1;
+  }
+  return n;
+}
+
+bool same_points(const Point* a, const Point* b, int n) {
+  for (int i = 0; i < n; ++i) {
+    if (a[i].inf != b[i].inf) return false;
+    if (!a[i].inf && !req(a[i].v, b[i].v)) return false;
+  }
+  return true;
+}
+
+std::string rat_str(Rat q) {
+  char buf[64];
+  if (q.d == 1) snprintf(buf, sizeof buf, "%lld", (long long)q.n);
+  else snprintf(buf, sizeof buf, "%lld/%lld", (long long)q.n, (long long)q.d);
+  return buf;
+}
+
+std::string transforms_json(const Transforms& t) {
+  std::string j = "{\"m\":" + std::to_string(t.m) + ",\"r\":" + std::to_string(t.r) +
+                  ",\"alpha\":" + std::to_string(t.a) + ",\"points\":[";
+  for (int k = 0; k < t.a; ++k) {
+    if (k) j += ",";
+    j += "\"" + (t.pts[k].inf ? std::string("inf") : rat_str(t.pts[k].v)) + "\"";
+  }
+  auto mat = [&](const char* name, const Rat (*M)[kMaxAlpha], int rows, int cols) {
+    j += std::string("],\"") + name + "\":[";
+    for (int i = 0; i < rows; ++i) {
+      if (i) j += ",";
+      j += "[";
+      for (int c = 0; c < cols; ++c) {
+        if (c) j += ",";
+        j += "\"" + rat_str(M[i][c]) + "\"";
+      }
+      j += "]";
+    }
+  };
+  mat("AT", t.AT, t.m, t.a);
+  mat("G", t.G, t.a, t.r);
+  mat("BT", t.BT, t.a, t.a);
+  j += "]}";
+  return j;
+}
+
+wino_status synth_checked(int m, int r, const char* points, Transforms& t, int& spec) {
+  if (m < 1 || r < 1) return fail(WINO_ERR_ARG, "m and r must be >= 1 (m=%d r=%d)", m, r);
+  const int a = m + r - 1;
+  if (a > kMaxAlpha) return fail(WINO_ERR_UNSUPPORTED, "alpha = m + r - 1 = %d exceeds %d", a, kMaxAlpha);
+  Point pts[kMaxAlpha]{};
+  Point def[kMaxAlpha]{}, seq[kMaxAlpha]{};
+  default_points(a, kPsDefault, def);
+  const bool have_seq = default_points(a, kPsSeq, seq) == 0;
+  if (points == nullptr || *points == 0) {
+    for (int i = 0; i < a; ++i) pts[i] = def[i];
+  } else {
+    const int n = parse_points(points, pts, kMaxAlpha);
+    if (n < 0) return fail(WINO_ERR_POINTS, "cannot parse points \"%s\"", points);
+    if (n != a) return fail(WINO_ERR_POINTS, "need alpha = m + r - 1 = %d points, got %d", a, n);
+  }
+  t = synthesize(m, r, pts);
+  if (t.err == 3) return fail(WINO_ERR_POINTS, "points must be distinct with at most one infinity");
+  if (t.err) return fail(WINO_ERR_SYNTH, "exact synthesis/identity check failed for F(%d,%d)", m, r);
+  spec = kSpecRuntime;
+  if (r == 3 && (m == 2 || m == 4)) {
+    if (same_points(pts, def, a)) spec = kSpecDefault;
+    else if (have_seq && same_points(pts, seq, a)) spec = kSpecSeq;
+  }
+  return WINO_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+constexpr int kMaxProf = 4096;
+
+}  // namespace
+
+struct wino_plan_s {
+  int N = 0, m = 0, r = 0, a = 0, C = 0, K = 0, batch = 0, gemm_mode = 0, fuse = 0, device = 0, spec = 0;
+  int64_t in[kMaxN]{}, out[kMaxN]{};
+  int pad[kMaxN]{}, tiles[kMaxN]{};
+  int64_t Tps = 0, T_s = 0, P = 0, K_s = 0;
+  Transforms tf{};
+  XfParams xp{};
+  FParams fp{};
+  KGeom geom{};
+  float* ubuf = nullptr;  // U_hi | U_lo | (U32)
+  float *Uhi = nullptr, *Ulo = nullptr, *U32 = nullptr;
+  size_t filter_bytes = 0, filter_bcast_bytes = 0;
+  float *V = nullptr, *M = nullptr;
+  size_t ws_bytes = 0;
+  float *x_dev = nullptr, *y_dev = nullptr;
+  bool filter_ready = false;
+  TcGemm tg{};
+  bool prof = false;
+  int prof_calls = 0;
+  std::vector<cudaEvent_t> ev;  // 4 per recorded call
+  double prof_ms[3] = {0, 0, 0};
+  int prof_read = 0;
+};
+
+extern "C" {
+
+const char* wino_last_error(void) { return g_err.c_str(); }
+const char* wino_version(void) { return "wino-nd-b200 0.1 (sm_100a)"; }
+
+wino_status wino_synthesize(int m, int r, const char* points, double* AT, double* G, double* BT, char* json,
+                            size_t cap) {
+  Transforms t;
+  int spec;
+  wino_status st = synth_checked(m, r, points, t, spec);
+  if (st) return st;
+  const int a = t.a;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < a; ++j)
+      if (AT) AT[i * a + j] = rat_to_f64(t.AT[i][j]);
+  for (int i = 0; i < a; ++i)
+    for (int j = 0; j < r; ++j)
+      if (G) G[i * r + j] = rat_to_f64(t.G[i][j]);
+  for (int i = 0; i < a; ++i)
+    for (int j = 0; j < a; ++j)
+      if (BT) BT[i * a + j] = rat_to_f64(t.BT[i][j]);
+  if (json && cap) {
+    const std::string s = transforms_json(t);
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    memcpy(json, s.data(), n);
+    json[n] = 0;
+  }
+  return WINO_OK;
+}
+
+wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dims, int m, int r, int C, int K,
+                                int batch, const int* padding, const char* points, int gemm_mode, int fuse,
+                                int device) {
+  if (!plan_out) return fail(WINO_ERR_ARG, "plan pointer is NULL");
+  *plan_out = nullptr;
+  if (N < 1 || N > kMaxN) return fail(WINO_ERR_ARG, "N must be in 1..4 (got %d)", N);
+  if (!dims) return fail(WINO_ERR_ARG, "dims is NULL");
+  if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
+  if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
+  if (fuse != 0) return fail(WINO_ERR_UNSUPPORTED, "fuse bitmask %d not implemented in this build", fuse);
+  Transforms t;
+  int spec;
+  wino_status st = synth_checked(m, r, points, t, spec);
+  if (st) return st;
+  const int a = t.a;
+  if (a > kMaxA || !xform_supported(N, a, m, spec))
+    return fail(WINO_ERR_UNSUPPORTED, "no device transform kernels for N=%d alpha=%d m=%d", N, a, m);
+
+  wino_plan_s* p = new wino_plan_s();
+  p->N = N; p->m = m; p->r = r; p->a = a; p->C = C; p->K = K; p->batch = batch;
+  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? WINO_GEMM_3XTF32 : gemm_mode;
+  p->fuse = fuse;
+  p->spec = spec;
+  p->tf = t;
+  int64_t Tps = 1;
+  for (int n = 0; n < N; ++n) {
+    p->in[n] = dims[n];
+    p->pad[n] = padding ? padding[n] : 0;
+    if (dims[n] < 1 || p->pad[n] < 0) { delete p; return fail(WINO_ERR_ARG, "dims must be >= 1 and padding >= 0"); }
+    p->out[n] = dims[n] + 2 * p->pad[n] - r + 1;
+    if (p->out[n] < 1) { delete p; return fail(WINO_ERR_SHAPE, "kernel %d larger than padded input %lld on axis %d", r, (long long)(dims[n] + 2 * p->pad[n]), n); }
+    p->tiles[n] = (int)((p->out[n] + m - 1) / m);
+    Tps *= p->tiles[n];
+  }
+  p->Tps = Tps;
+  const int64_t T = Tps * batch;
+  if (T > (int64_t)INT32_MAX - 256) { delete p; return fail(WINO_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)T); }
+  p->T_s = (T + 127) / 128 * 128;
+  p->P = ipow(a, N);
+  const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32;
+  const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+  p->K_s = tc ? (K + bn - 1) / bn * bn : (K + 31) / 32 * 32;
+
+  // tables
+  const FloatTables ft = to_tables(t);
+  for (int i = 0; i < kMaxA; ++i)
+    for (int j = 0; j < kMaxA; ++j) {
+      p->xp.AT[i][j] = ft.AT[i][j];
+      p->xp.BT[i][j] = ft.BT[i][j];
+      p->fp.G[i][j] = ft.G[i][j];
+    }
+  p->fp.N = N; p->fp.a = a; p->fp.r = r; p->fp.C = C; p->fp.K = K; p->fp.K_s = (int)p->K_s; p->fp.P = p->P;
+
+  KGeom& g = p->geom;
+  int64_t sin = 1, sout = 1;
+  for (int n = N - 1; n >= 0; --n) {
+    g.in[n] = p->in[n]; g.out[n] = p->out[n]; g.tiles[n] = p->tiles[n]; g.pad[n] = p->pad[n];
+    g.in_stride[n] = sin; g.out_stride[n] = sout;
+    sin *= p->in[n]; sout *= p->out[n];
+  }
+  g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m;
+
+  // device buffers
+  if (device < 0) {
+    if (cudaGetDevice(&device) != cudaSuccess) { delete p; return fail(WINO_ERR_CUDA, "no CUDA device"); }
+  }
+  p->device = device;
+  DeviceGuard guard(device);
+  const size_t ucount = (size_t)p->P * C * p->K_s;
+  const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
+  p->filter_bytes = ucount * 4 * nbuf;
+  p->ws_bytes = ((size_t)p->P * C * p->T_s + (size_t)p->P * K * p->T_s) * 4;
+  cudaError_t e = cudaMalloc(&p->ubuf, p->filter_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->V, p->ws_bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p->ubuf);
+    delete p;
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? WINO_ERR_NOMEM : WINO_ERR_CUDA, "device allocation failed: %s",
+                cudaGetErrorString(e));
+  }
+  p->M = p->V + (size_t)p->P * C * p->T_s;
+  if (p->gemm_mode == WINO_GEMM_FFMA) {
+    p->U32 = p->ubuf;
+  } else {
+    p->Uhi = p->ubuf;
+    p->Ulo = p->ubuf + ucount;
+  }
+  p->filter_bcast_bytes = p->filter_bytes;
+  if (tc) {
+    e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
+                        p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
+    if (e != cudaSuccess) {
+      wino_plan_destroy(p);
+      return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *plan_out = p;
+  return WINO_OK;
+}
+
+wino_status wino_plan_create(wino_plan_t* plan, int N, const int64_t* dims, int m, int r, int C, int K, int batch,
+                             const int* padding) {
+  return wino_plan_create_ex(plan, N, dims, m, r, C, K, batch, padding, nullptr, WINO_GEMM_AUTO, 0, -1);
+}
+
+wino_status wino_plan_destroy(wino_plan_t p) {
+  if (!p) return WINO_OK;
+  DeviceGuard guard(p->device);
+  cudaFree(p->ubuf);
+  cudaFree(p->V);
+  cudaFree(p->x_dev);
+  cudaFree(p->y_dev);
+  for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+  delete p;
+  return WINO_OK;
+}
+
+wino_status wino_filter_transform(wino_plan_t p, const float* g, wino_stream_t stream) {
+  if (!p || !g) return fail(WINO_ERR_ARG, "NULL plan or filter pointer");
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_filter_xform(g, p->Uhi, p->Ulo, p->U32, p->fp, (cudaStream_t)stream));
+  p->filter_ready = true;
+  return WINO_OK;
+}
+
+static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, cudaStream_t s) {
+  KGeom g = p->geom;
+  g.T = (int64_t)B * p->Tps;
+  const bool rec = p->prof && p->prof_calls < kMaxProf;
+  cudaEvent_t* ev = nullptr;
+  if (rec) {
+    const size_t need = 4 * (size_t)(p->prof_calls + 1);
+    while (p->ev.size() < need) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      p->ev.push_back(e);
+    }
+    ev = &p->ev[4 * (size_t)p->prof_calls];
+    CUDA_TRY(cudaEventRecord(ev[0], s));
+  }
+  CUDA_TRY(launch_xform(true, p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, s));
+  if (rec) CUDA_TRY(cudaEventRecord(ev[1], s));
+  if (p->gemm_mode == WINO_GEMM_FFMA) {
+    CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, (int)p->K_s, s));
+  } else {
+    CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, s));
+  }
+  if (rec) CUDA_TRY(cudaEventRecord(ev[2], s));
+  CUDA_TRY(launch_xform(false, p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
+  if (rec) {
+    CUDA_TRY(cudaEventRecord(ev[3], s));
+    ++p->prof_calls;
+  }
+  return WINO_OK;
+}
+
+wino_status wino_forward(wino_plan_t p, const float* x, float* y, int B, wino_stream_t stream) {
+  if (!p || !x || !y) return fail(WINO_ERR_ARG, "NULL plan, x or y");
+  if (B < 1 || B > p->batch) return fail(WINO_ERR_ARG, "B=%d outside 1..%d (planned batch)", B, p->batch);
+  if (!p->filter_ready) return fail(WINO_ERR_STATE, "forward before wino_filter_transform / mark_ready");
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaGetLastError());
+  return forward_impl(p, x, y, B, (cudaStream_t)stream);
+}
+
+wino_status wino_forward_host(wino_plan_t p, const float* x_host, float* y_host, int B, wino_stream_t stream) {
+  if (!p || !x_host || !y_host) return fail(WINO_ERR_ARG, "NULL plan, x_host or y_host");
+  if (B < 1 || B > p->batch) return fail(WINO_ERR_ARG, "B=%d outside 1..%d (planned batch)", B, p->batch);
+  if (!p->filter_ready) return fail(WINO_ERR_STATE, "forward before wino_filter_transform / mark_ready");
+  DeviceGuard guard(p->device);
+  const size_t xb = (size_t)p->batch * p->C * p->geom.in_vol * 4;
+  const size_t yb = (size_t)p->batch * p->K * p->geom.out_vol * 4;
+  if (!p->x_dev) CUDA_TRY(cudaMalloc(&p->x_dev, xb));
+  if (!p->y_dev) CUDA_TRY(cudaMalloc(&p->y_dev, yb));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t xn = (size_t)B * p->C * p->geom.in_vol * 4;
+  const size_t yn = (size_t)B * p->K * p->geom.out_vol * 4;
+  CUDA_TRY(cudaMemcpyAsync(p->x_dev, x_host, xn, cudaMemcpyHostToDevice, s));
+  wino_status st = forward_impl(p, p->x_dev, p->y_dev, B, s);
+  if (st) return st;
+  CUDA_TRY(cudaMemcpyAsync(y_host, p->y_dev, yn, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return WINO_OK;
+}
+
+wino_status wino_plan_out_dims(wino_plan_t p, int64_t* out) {
+  if (!p || !out) return fail(WINO_ERR_ARG, "NULL argument");
+  for (int n = 0; n < p->N; ++n) out[n] = p->out[n];
+  return WINO_OK;
+}
+
+wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  if (ws) *ws = p->ws_bytes;
+  if (fb) *fb = p->filter_bytes;
+  return WINO_OK;
+}
+
+wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
+  if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
+  const int64_t v[16] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+                         p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->spec};
+  memcpy(info, v, sizeof v);
+  return WINO_OK;
+}
+
+wino_status wino_filter_buffer(wino_plan_t p, void** dev_ptr, size_t* bytes) {
+  if (!p || !dev_ptr || !bytes) return fail(WINO_ERR_ARG, "NULL argument");
+  *dev_ptr = p->ubuf;
+  *bytes = p->filter_bcast_bytes;
+  return WINO_OK;
+}
+
+wino_status wino_filter_mark_ready(wino_plan_t p) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  p->filter_ready = true;
+  return WINO_OK;
+}
+
+wino_status wino_workspace(wino_plan_t p, void** V, void** M) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  if (V) *V = p->V;
+  if (M) *M = p->M;
+  return WINO_OK;
+}
+
+wino_status wino_profile_enable(wino_plan_t p, int enable) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  p->prof = enable != 0;
+  p->prof_calls = 0;
+  return WINO_OK;
+}
+
+wino_status wino_profile_read(wino_plan_t p, double* ms, int* calls) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  DeviceGuard guard(p->device);
+  double acc[3] = {0, 0, 0};
+  for (int c = 0; c < p->prof_calls; ++c) {
+    cudaEvent_t* e = &p->ev[4 * (size_t)c];
+    CUDA_TRY(cudaEventSynchronize(e[3]));
+    for (int s = 0; s < 3; ++s) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, e[s], e[s + 1]));
+      acc[s] += t;
+    }
+  }
+  if (ms) for (int s = 0; s < 3; ++s) ms[s] = acc[s];
+  if (calls) *calls = p->prof_calls;
+  return WINO_OK;
+}
+
+wino_status wino_get_transforms(wino_plan_t p, double* AT, double* G, double* BT, char* json, size_t cap) {
+  if (!p) return fail(WINO_ERR_ARG, "NULL plan");
+  const Transforms& t = p->tf;
+  const int a = t.a, m = t.m, r = t.r;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < a; ++j)
+      if (AT) AT[i * a + j] = rat_to_f64(t.AT[i][j]);
+  for (int i = 0; i < a; ++i)
+    for (int j = 0; j < r; ++j)
+      if (G) G[i * r + j] = rat_to_f64(t.G[i][j]);
+  for (int i = 0; i < a; ++i)
+    for (int j = 0; j < a; ++j)
+      if (BT) BT[i * a + j] = rat_to_f64(t.BT[i][j]);
+  if (json && cap) {
+    const std::string s = transforms_json(t);
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    memcpy(json, s.data(), n);
+    json[n] = 0;
+  }
+  return WINO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+"""Thin ctypes binding of libwino.so (include/wino.h).
+
+Argument marshalling only: every stage of the layer runs in the CUDA kernels
+behind the C ABI.  The module-level functions carry the C names
+(``wino_plan_create``, ``wino_filter_transform``, ``wino_forward``, ...);
+``Plan`` is a convenience wrapper over them.  Tensors are torch CUDA tensors
+(fp32, contiguous) and are passed as raw device pointers; PyTorch provides
+device memory and streams only.
+
+There is no fallback: if libwino.so is missing or fails to load this module
+raises, and a call on a machine without a usable device returns
+WINO_ERR_CUDA through the ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+from pathlib import Path
+from typing import Optional, Sequence
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libwino.so"
+
+WINO_OK, WINO_ERR_ARG, WINO_ERR_SHAPE, WINO_ERR_POINTS, WINO_ERR_SYNTH = 0, 1, 2, 3, 4
+WINO_ERR_STATE, WINO_ERR_UNSUPPORTED, WINO_ERR_CUDA, WINO_ERR_NOMEM = 5, 6, 7, 8
+STATUS_NAMES = {0: "WINO_OK", 1: "WINO_ERR_ARG", 2: "WINO_ERR_SHAPE", 3: "WINO_ERR_POINTS",
+                4: "WINO_ERR_SYNTH", 5: "WINO_ERR_STATE", 6: "WINO_ERR_UNSUPPORTED",
+                7: "WINO_ERR_CUDA", 8: "WINO_ERR_NOMEM"}
+WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32 = 0, 1, 2, 3
+WINO_FUSE_NONE, WINO_FUSE_L2_CHUNK = 0, 4
+
+EXPORTS = ["wino_plan_create", "wino_plan_create_ex", "wino_plan_destroy", "wino_filter_transform",
+           "wino_forward", "wino_forward_host", "wino_plan_out_dims", "wino_plan_sizes",
+           "wino_plan_info", "wino_filter_buffer", "wino_filter_mark_ready", "wino_workspace",
+           "wino_profile_enable", "wino_profile_read", "wino_synthesize", "wino_get_transforms",
+           "wino_last_error", "wino_version"]
+
+
+class WinoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libwino.so (build it first with paper_1611_06565_b200._build)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError("libwino.so not built: run `python -m paper_1611_06565_b200._build` "
+                              "(or __graft_entry__.build())")
+        L = ctypes.CDLL(str(LIB_PATH))
+        vp, i64p, i32p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)
+        sz, szp, dp = ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_double)
+        c_int = ctypes.c_int
+        sig = {
+            "wino_plan_create": [ctypes.POINTER(vp), c_int, i64p, c_int, c_int, c_int, c_int, c_int, i32p],
+            "wino_plan_create_ex": [ctypes.POINTER(vp), c_int, i64p, c_int, c_int, c_int, c_int, c_int,
+                                    i32p, ctypes.c_char_p, c_int, c_int, c_int],
+            "wino_plan_destroy": [vp],
+            "wino_filter_transform": [vp, vp, vp],
+            "wino_forward": [vp, vp, vp, c_int, vp],
+            "wino_forward_host": [vp, vp, vp, c_int, vp],
+            "wino_plan_out_dims": [vp, i64p],
+            "wino_plan_sizes": [vp, szp, szp],
+            "wino_plan_info": [vp, i64p],
+            "wino_filter_buffer": [vp, ctypes.POINTER(vp), szp],
+            "wino_filter_mark_ready": [vp],
+            "wino_workspace": [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)],
+            "wino_profile_enable": [vp, c_int],
+            "wino_profile_read": [vp, dp, i32p],
+            "wino_synthesize": [c_int, c_int, ctypes.c_char_p, dp, dp, dp, ctypes.c_char_p, sz],
+            "wino_get_transforms": [vp, dp, dp, dp, ctypes.c_char_p, sz],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = c_int
+        L.wino_last_error.restype = ctypes.c_char_p
+        L.wino_last_error.argtypes = []
+        L.wino_version.restype = ctypes.c_char_p
+        L.wino_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(st: int) -> None:
+    if st != WINO_OK:
+        raise WinoError(st, lib().wino_last_error().decode())
+
+
+def _i64arr(v):
+    return (ctypes.c_int64 * len(v))(*[int(a) for a in v])
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev_ptr(t, name):
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("%s must be a contiguous CUDA tensor" % name)
+    import torch
+    if t.dtype != torch.float32:
+        raise ValueError("%s must be float32" % name)
+    return t.data_ptr()
+
+
+# ------------------------------------------------------------- C-named calls
+def wino_version() -> str:
+    return lib().wino_version().decode()
+
+
+def wino_last_error() -> str:
+    return lib().wino_last_error().decode()
+
+
+def wino_synthesize(m: int, r: int, points: Optional[str] = None) -> dict:
+    """Host-only exact synthesis: dict with exact rational strings and doubles."""
+    a = m + r - 1
+    AT = (ctypes.c_double * (m * a))()
+    G = (ctypes.c_double * (a * r))()
+    BT = (ctypes.c_double * (a * a))()
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().wino_synthesize(m, r, points.encode() if points else None, AT, G, BT, buf, len(buf)))
+    d = json.loads(buf.value.decode())
+    d["AT_f64"] = [list(AT[i * a:(i + 1) * a]) for i in range(m)]
+    d["G_f64"] = [list(G[i * r:(i + 1) * r]) for i in range(a)]
+    d["BT_f64"] = [list(BT[i * a:(i + 1) * a]) for i in range(a)]
+    return d
+
+
+def wino_plan_create_ex(N, dims, m, r, C, K, batch, padding=None, points=None, gemm_mode=0, fuse=0,
+                        device=-1) -> int:
+    h = ctypes.c_void_p()
+    pad = (ctypes.c_int * N)(*([0] * N if padding is None else [int(p) for p in padding]))
+    _check(lib().wino_plan_create_ex(ctypes.byref(h), int(N), _i64arr(dims), int(m), int(r), int(C),
+                                     int(K), int(batch), pad, points.encode() if points else None,
+                                     int(gemm_mode), int(fuse), int(device)))
+    return h.value
+
+
+def wino_plan_create(N, dims, m, r, C, K, batch, padding=None) -> int:
+    h = ctypes.c_void_p()
+    pad = (ctypes.c_int * N)(*([0] * N if padding is None else [int(p) for p in padding]))
+    _check(lib().wino_plan_create(ctypes.byref(h), int(N), _i64arr(dims), int(m), int(r), int(C), int(K),
+                                  int(batch), pad))
+    return h.value
+
+
+def wino_plan_destroy(plan: int) -> None:
+    _check(lib().wino_plan_destroy(plan))
+
+
+def wino_filter_transform(plan: int, g, stream=None) -> None:
+    _check(lib().wino_filter_transform(plan, _dev_ptr(g, "g"), _stream_ptr(stream)))
+
+
+def wino_forward(plan: int, x, y, B: int, stream=None) -> None:
+    _check(lib().wino_forward(plan, _dev_ptr(x, "x"), _dev_ptr(y, "y"), int(B), _stream_ptr(stream)))
+
+
+def wino_forward_host(plan: int, x_host, y_host, B: int, stream=None) -> None:
+    """x_host / y_host: CPU float32 contiguous tensors (pin_memory() for speed)."""
+    import torch
+    for t, n in ((x_host, "x_host"), (y_host, "y_host")):
+        if t.is_cuda or not t.is_contiguous() or t.dtype != torch.float32:
+            raise ValueError("%s must be a contiguous CPU float32 tensor" % n)
+    _check(lib().wino_forward_host(plan, x_host.data_ptr(), y_host.data_ptr(), int(B), _stream_ptr(stream)))
+
+
+def wino_plan_out_dims(plan: int, N: int):
+    out = (ctypes.c_int64 * N)()
+    _check(lib().wino_plan_out_dims(plan, out))
+    return tuple(out)
+
+
+def wino_plan_sizes(plan: int):
+    ws, fb = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().wino_plan_sizes(plan, ctypes.byref(ws), ctypes.byref(fb)))
+    return ws.value, fb.value
+
+
+INFO_KEYS = ["N", "m", "r", "alpha", "C", "K", "batch", "T_per_sample", "T_stride", "n_points", "K_stride",
+             "gemm_mode", "fuse", "n_blk", "k_chunk", "specialised"]
+
+
+def wino_plan_info(plan: int) -> dict:
+    info = (ctypes.c_int64 * 16)()
+    _check(lib().wino_plan_info(plan, info))
+    return dict(zip(INFO_KEYS, list(info)))
+
+
+def wino_filter_buffer(plan: int):
+    p, n = ctypes.c_void_p(), ctypes.c_size_t()
+    _check(lib().wino_filter_buffer(plan, ctypes.byref(p), ctypes.byref(n)))
+    return p.value, n.value
+
+
+def wino_filter_mark_ready(plan: int) -> None:
+    _check(lib().wino_filter_mark_ready(plan))
+
+
+def wino_workspace(plan: int):
+    v, m = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib().wino_workspace(plan, ctypes.byref(v), ctypes.byref(m)))
+    return v.value, m.value
+
+
+def wino_profile_enable(plan: int, enable: bool = True) -> None:
+    _check(lib().wino_profile_enable(plan, int(bool(enable))))
+
+
+def wino_profile_read(plan: int):
+    ms = (ctypes.c_double * 3)()
+    calls = ctypes.c_int()
+    _check(lib().wino_profile_read(plan, ms, ctypes.byref(calls)))
+    return list(ms), calls.value
+
+
+def wino_get_transforms(plan: int) -> dict:
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().wino_get_transforms(plan, None, None, None, buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+# ------------------------------------------------------------- torch views
+class _CAI:
+    def __init__(self, ptr, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def device_view(ptr: int, shape, device=None):
+    """A torch CUDA float32 tensor aliasing plan-owned device memory."""
+    import torch
+    return torch.as_tensor(_CAI(ptr, shape), device=device or "cuda")
+
+
+# ------------------------------------------------------------- Plan
+class Plan:
+    """One N-D Winograd conv layer F(m^N, r^N) on one GPU.
+
+    Plan(N, dims, m, r, C, K, batch, padding=None, points=None, gemm_mode=0, fuse=0, device=-1)
+    """
+
+    def __init__(self, N: int, dims: Sequence[int], m: int, r: int, C: int, K: int, batch: int,
+                 padding: Optional[Sequence[int]] = None, points: Optional[str] = None,
+                 gemm_mode: int = WINO_GEMM_AUTO, fuse: int = 0, device: int = -1):
+        self.N, self.dims, self.m, self.r, self.C, self.K, self.batch = N, tuple(dims), m, r, C, K, batch
+        self.padding = tuple(padding) if padding is not None else (0,) * N
+        self.h = wino_plan_create_ex(N, dims, m, r, C, K, batch, self.padding, points, gemm_mode, fuse, device)
+        self.out_dims = wino_plan_out_dims(self.h, N)
+        self.info = wino_plan_info(self.h)
+
+    def filter_transform(self, g, stream=None) -> None:
+        wino_filter_transform(self.h, g, stream)
+
+    def forward(self, x, y=None, stream=None):
+        import torch
+        B = x.shape[0]
+        if y is None:
+            y = torch.empty((B, self.K) + tuple(self.out_dims), device=x.device, dtype=torch.float32)
+        wino_forward(self.h, x, y, B, stream)
+        return y
+
+    def forward_host(self, x_host, y_host, stream=None) -> None:
+        wino_forward_host(self.h, x_host, y_host, x_host.shape[0], stream)
+
+    def filter_tensor(self):
+        """The U buffer (U_hi | U_lo) as a flat float32 CUDA tensor (for NCCL broadcast)."""
+        ptr, nbytes = wino_filter_buffer(self.h)
+        return device_view(ptr, (nbytes // 4,))
+
+    def mark_ready(self) -> None:
+        wino_filter_mark_ready(self.h)
+
+    def workspace(self):
+        """(V [P][C][T_s], M [P][K][T_s]) views of the unfused workspace."""
+        v, m = wino_workspace(self.h)
+        P, Ts = self.info["n_points"], self.info["T_stride"]
+        return device_view(v, (P, self.C, Ts)), device_view(m, (P, self.K, Ts))
+
+    def transforms(self) -> dict:
+        return wino_get_transforms(self.h)
+
+    def profile(self, enable=True):
+        wino_profile_enable(self.h, enable)
+
+    def profile_read(self):
+        return wino_profile_read(self.h)
+
+    def sizes(self):
+        return wino_plan_sizes(self.h)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            wino_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
