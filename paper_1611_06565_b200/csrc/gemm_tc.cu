@@ -10,7 +10,8 @@
 // of 128 tiles x BN output channels; units are ordered xi-major so concurrently
 // running CTAs share U_xi in L2.
 //   warp 8      TMA producer: V tile (fp32, 128 x kc) + U_hi/U_lo tiles (BN x kc)
-//               into a `stages`-deep smem ring, SWIZZLE_128B, MN-major.
+//               into a `stages`-deep smem ring, MN-major, 128B rows with
+//               32-byte swizzle atoms (SWIZZLE_128B_BASE32B).
 //   warps 0-3   converter: split the V tile in place into V_hi and V_lo (the
 //               tf32 rounding must be explicit: the tensor core truncates).
 //   warp 9      MMA issuer (one thread): 3 x (kc/8) tcgen05.mma.kind::tf32
@@ -27,6 +28,10 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int kThreads = 320;
+
+// Debug dump (dev only; set through tc_set_debug): CTA 0 copies its first
+// smem stage after conversion and the raw accumulator of its first unit.
+__device__ float* g_dbg = nullptr;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -74,17 +79,22 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d, uint64_t a, uint64_t b, 
       : "memory");
 }
 
-// Shared-memory matrix descriptor, SWIZZLE_128B canonical MN-major layout:
-// atoms of 32 (MN) x 8 (K) fp32 = 1024 B; LBO = byte distance between atoms
-// along MN, SBO = between atoms along K (bits: addr>>4 [0,14), LBO>>4
-// [16,30), SBO>>4 [32,46), version 1 [46,48), layout SWIZZLE_128B=2 [61,64)).
+// Shared-memory matrix descriptor for the canonical MN-major tf32 layout
+// SWIZZLE_128B_BASE32B (layout type 1; fp32 MN-major operands require the
+// 32-byte swizzle base): rows of 128 B = 32 MN elements, 32-byte chunks XORed
+// with (row mod 4), 4 K-rows (512 B) per swizzle atom.
+//   LBO = byte distance between 32-element groups along MN,
+//   SBO = byte distance between 4-row atoms along K (512 when dense).
+// Bits: addr>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
+// layout type [61,64).  The TMA side writes the same pattern with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
   return d;
 }
 
@@ -212,11 +222,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           for (int j = 0; j < kc / 8; ++j) {
             const uint32_t off = (uint32_t)j * 1024u;
             const uint32_t accum = (ch | j) != 0;
-            const uint64_t dah = sdesc(a_hi + off, lbo, 1024u);
-            const uint64_t dbh = sdesc(b_hi + off, lbo, 1024u);
+            const uint64_t dah = sdesc(a_hi + off, lbo, 512u);
+            const uint64_t dbh = sdesc(b_hi + off, lbo, 512u);
             if (three) {
-              tc_mma_tf32(d, sdesc(a_lo + off, lbo, 1024u), dbh, idesc, accum);
-              tc_mma_tf32(d, dah, sdesc(b_lo + off, lbo, 1024u), idesc, 1u);
+              tc_mma_tf32(d, sdesc(a_lo + off, lbo, 512u), dbh, idesc, accum);
+              tc_mma_tf32(d, dah, sdesc(b_lo + off, lbo, 512u), idesc, 1u);
               tc_mma_tf32(d, dah, dbh, idesc, 1u);
             } else {
               tc_mma_tf32(d, dah, dbh, idesc, accum);
@@ -251,6 +261,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (g_dbg && blockIdx.x == 0 && u == blockIdx.x && ch == 0) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const float* sp = reinterpret_cast<const float*>(smem + s * stage_bytes);
+          for (uint32_t i = threadIdx.x; i < stage_bytes / 4; i += 128) g_dbg[i] = sp[i];
+        }
         mbar_arrive(conv(s));
         if (++s == stages) { s = 0; ph ^= 1u; }
       }
@@ -271,6 +286,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         const int k0 = nb * BN + cb * 32;
+        if (g_dbg && blockIdx.x == 0 && u == blockIdx.x) {
+          for (int j = 0; j < 32; ++j) g_dbg[65536 + (q * 32 + lane) * 256 + cb * 32 + j] = __uint_as_float(r[j]);
+        }
         if (t < T) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -294,6 +312,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 }  // namespace tc
 
 // ---------------------------------------------------------------- host side
+cudaError_t tc_set_debug(float* p) { return cudaMemcpyToSymbol(tc::g_dbg, &p, sizeof(p)); }
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -319,7 +339,7 @@ static cudaError_t encode3d(CUtensorMap* tm, const float* base, int64_t inner_s,
   cuuint32_t box[3] = {32, (cuuint32_t)kc, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }

@@ -32,6 +32,7 @@ struct TcGemm {
 };
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,
                             int64_t T_s, int C, int K_s, int K, int three, int device);
+cudaError_t tc_set_debug(float* p);
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s);
 

@@ -474,6 +474,20 @@ wino_status wino_profile_read(wino_plan_t p, double* ms, int* calls) {
   return WINO_OK;
 }
 
+// Dev-only (not in wino.h): allocate / return the tcgen05 debug dump buffer.
+WINO_API wino_status wino_debug_tc_dump(void** ptr, size_t* bytes) {
+  static float* buf = nullptr;
+  const size_t n = (65536 + 128 * 256) * sizeof(float);
+  if (!buf) {
+    CUDA_TRY(cudaMalloc(&buf, n));
+    CUDA_TRY(cudaMemset(buf, 0, n));
+    CUDA_TRY(tc_set_debug(buf));
+  }
+  *ptr = buf;
+  *bytes = n;
+  return WINO_OK;
+}
+
 wino_status wino_get_transforms(wino_plan_t p, double* AT, double* G, double* BT, char* json, size_t cap) {
   if (!p) return fail(WINO_ERR_ARG, "NULL plan");
   const Transforms& t = p->tf;
