@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- N-D Winograd conv layer F(m^N, r^N) on B200 (arXiv 1611.06565).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2] [--extra c3,c4,c5] [--scaling weak|strong]
+
+Metric (BASELINE.json): direct-convolution-equivalent TFLOP/s and ms per layer.
+A step is one full forward of the layer (stages a2 input transform -> a3
+per-point GEMM -> a4 output transform) over one batch that is already
+resident in HBM; the filter transform a1 runs once per weight set (the
+paper caches transformed kernels) and is reported separately.
+The headline workload is BASELINE.json configs[1] (c2); the other configs
+are reported under "configs".  L2 is flushed (256 MiB memset) between timed
+steps, outside the per-step CUDA events.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): the batch shards with no
+per-forward collective; rank 0 transforms the filters and broadcasts U once
+(SURVEY.md 8(e)).  "weak" (default): every rank convolves a full config-size
+batch; "strong": the config batch is split.  Time = max over ranks.
+
+--impl reference times the CPU float64 oracle (oracle/, the only reference
+that exists for this paper) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "direct-equiv TFLOP/s and ms per N-D Winograd conv layer at 1/2/4/8 B200"
+GUIDE_TF32_OVER_BF16 = 1.1 / 2.25          # B200_PROFILING.md nominal dense ratio
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--extra", default="c3,c4,c5", help="comma list of further configs ('' for none)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"],
+                "bf16_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
+                except ValueError:
+                    pass
+        os.unlink(self.path)
+        if not rows:
+            return out
+        busy = [r for r in rows if r[2] >= 30.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i, v in enumerate(r[3]) if v.lower().startswith("active")})
+        out.update(sm_mhz=statistics.median(r[0] for r in busy), sm_max_mhz=max(r[1] for r in rows),
+                   reasons=reasons, samples=len(busy))
+        return out
+
+
+# ------------------------------------------------------------------ helpers
+def stage_bytes(cfg, B):
+    """Algorithmic (compulsory) bytes of each stage for B samples."""
+    T = cfg.tiles(B)
+    P = cfg.alpha ** cfg.N
+    x = B * cfg.C * math.prod(cfg.dims) * 4
+    y = B * cfg.K * math.prod(cfg.out_dims) * 4
+    V = P * cfg.C * T * 4
+    M = P * cfg.K * T * 4
+    U = P * cfg.C * cfg.K * 4
+    return {"input_xform": x + V, "gemm": V + U + M, "output_xform": M + y}
+
+
+def roofline_for(cfg, B, stage, ms, peaks):
+    t = ms * 1e-3
+    nbytes = stage_bytes(cfg, B)[stage]
+    tf32 = peaks["bf16"] * GUIDE_TF32_OVER_BF16
+    if stage == "gemm":
+        flops = cfg.winograd_gemm_flops(B)
+        t_mem = nbytes / (peaks["hbm_gbs"] * 1e9)
+        t_tc = flops / (tf32 / 3 * 1e12)
+        if t_tc > t_mem:
+            ach = flops / t / 1e12
+            return {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32 / 3, 1), "unit": "TFLOP/s",
+                    "frac": round(ach / (tf32 / 3), 4), "traffic": None,
+                    "note": "fp32 flops of the per-point GEMM vs 3xTF32 fp32-equivalent peak = "
+                            "(bf16 %s x 1.1/2.25) / 3" % peaks["source"]}
+    ach = nbytes / t / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None}
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, cfg_names, rank, world, local, peaks):
+    import torch
+    import paper_1611_06565_b200 as pkg
+    from paper_1611_06565_b200 import dist as wdist
+    from paper_1611_06565_b200.workloads import CONFIGS, make_inputs
+
+    dev = torch.device("cuda", local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    results = {}
+    for name in cfg_names:
+        cfg = CONFIGS[name]
+        if args.scaling == "weak":
+            B = cfg.batch
+            x, g = make_inputs(cfg, seed=rank)
+            gref = make_inputs(cfg, seed=0)[1]
+            g = gref                                  # same weights on every rank
+        else:
+            lo, hi = wdist.shard_range(cfg.batch, rank, world)
+            B = hi - lo
+            xf, g = make_inputs(cfg, seed=0)
+            x = xf[lo:hi].contiguous()
+        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding, device=local)
+        stream = torch.cuda.current_stream(dev)
+        # a1 once per weight set on rank 0, U broadcast over NCCL to the others
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if rank == 0:
+            gd = g.to(dev)
+            e0.record(stream)
+            plan.filter_transform(gd, stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            filt_ms = e0.elapsed_time(e1)
+        else:
+            filt_ms = None
+        wdist.broadcast_filter(plan.filter_tensor(), src=0)
+        torch.cuda.synchronize(dev)
+        if rank != 0:
+            plan.mark_ready()
+        xd = x.to(dev)
+        y = torch.empty((B, cfg.K) + cfg.out_dims, device=dev, dtype=torch.float32)
+        for _ in range(max(args.warmup, 3)):
+            plan.forward(xd, y, stream)
+        torch.cuda.synchronize(dev)
+        # ---- timed region: K steps, barrier + sync on both sides
+        plan.profile(True)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        wdist.barrier(device=dev)
+        torch.cuda.synchronize(dev)
+        for i in range(args.steps):
+            flush.zero_()                              # L2 flush, outside the step events
+            evs[i][0].record(stream)
+            plan.forward(xd, y, stream)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        wdist.barrier(device=dev)
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        stage_ms, calls = plan.profile_read()
+        plan.profile(False)
+        ms_local = sum(step_ms) / len(step_ms)
+        ms = wdist.max_over_ranks(ms_local, device=dev)
+        stages = dict(zip(["input_xform", "gemm", "output_xform"], [s / calls for s in stage_ms]))
+        # ---- end to end through the public C ABI with host buffers
+        xh = x.pin_memory()
+        yh = torch.empty((B, cfg.K) + cfg.out_dims, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            plan.forward_host(xh, yh, stream)
+        wdist.barrier(device=dev)
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(max(3, min(args.steps, 20)))]
+        for a, b in ee:
+            a.record(stream)
+            plan.forward_host(xh, yh, stream)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = wdist.max_over_ranks(sum(a.elapsed_time(b) for a, b in ee) / len(ee), device=dev)
+        flops_rank = cfg.direct_flops(B)
+        res = {
+            "name": name, "cfg": cfg, "B": B, "ms": ms, "tflops": world * flops_rank / (ms * 1e-3) / 1e12,
+            "stages_ms": stages, "filter_ms": filt_ms, "e2e_ms": e2e_ms,
+            "e2e_tflops": world * flops_rank / (e2e_ms * 1e-3) / 1e12,
+            "h2d": xh.numel() * 4, "d2h": yh.numel() * 4, "launches": 3 * args.steps,
+            "info": plan.info,
+        }
+        results[name] = res
+        plan.close()
+        del xd, y
+        torch.cuda.empty_cache()
+    return results
+
+
+def cpu_baseline_sample(cfg, seconds):
+    """Time the float64 oracle (as it stands) on a bounded sample of the
+    workload: outputs computed one by one at random positions."""
+    import numpy as np
+    from oracle import direct
+    from paper_1611_06565_b200.workloads import make_inputs
+    x, g = make_inputs(cfg)
+    per_pt = 2 * cfg.C * cfg.r ** cfg.N
+    n_out = cfg.batch * cfg.K * math.prod(cfg.out_dims)
+    rng = np.random.default_rng(0)
+    xn, gn = x.numpy(), g.numpy()
+    npts = 4096
+    t0 = time.perf_counter()
+    direct.direct_conv_at(xn, gn, cfg.pad, rng.integers(0, n_out, npts))
+    dt = time.perf_counter() - t0
+    npts2 = int(min(n_out, max(npts, npts * (seconds * 0.8) / max(dt, 1e-3))))
+    idx = rng.integers(0, n_out, npts2)
+    t0 = time.perf_counter()
+    direct.direct_conv_at(xn, gn, cfg.pad, idx)
+    dt = time.perf_counter() - t0
+    return {"value": round(npts2 * per_pt / dt / 1e12, 6), "unit": "TFLOP/s", "cores": direct.num_threads(),
+            "kind": "oracle", "seconds": round(dt, 2),
+            "sample": "%d random outputs of %s (of %d), float64 direct correlation, OpenMP" % (npts2, cfg.name, n_out),
+            "ms_per_layer_extrapolated": round(cfg.direct_flops() / (npts2 * per_pt / dt) * 1e3, 1)}
+
+
+def cfg_dict(cfg, B, world, scaling):
+    return {"workload": "%s: %s" % (cfg.name, cfg.desc), "model": "N-D Winograd conv layer (synthetic)",
+            "N": cfg.N, "dims": list(cfg.dims), "C": cfg.C, "K": cfg.K, "kernel": cfg.r, "pad": cfg.pad,
+            "F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "per_gpu_batch": B,
+            "global_batch": B * world if scaling == "weak" else cfg.batch, "seq_len": None,
+            "parallelism": "dp%d (batch shards, U broadcast once)" % world,
+            "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate)",
+            "l2": "flushed: 256 MiB memset between timed steps, outside the per-step events"}
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1611_06565_b200.workloads import CONFIGS
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference(args, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+    names = [args.config] + [n for n in args.extra.split(",") if n and n != args.config]
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    res = run_ours(args, names, rank, world, local, peaks)
+    clocks = sampler.stop() if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        traffic = load_traffic()
+        head = res[args.config]
+        cfg = head["cfg"]
+        out = {"metric": METRIC, "value": round(head["tflops"], 3), "unit": "TFLOP/s", "n_gpus": world,
+               "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(head["ms"], 5),
+               "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (seeded, BASELINE.json distributions; no dataset)",
+               "config": cfg_dict(cfg, head["B"], world, args.scaling)}
+        configs = {}
+        for name, r in res.items():
+            st = r["stages_ms"]
+            dom = max(st, key=st.get)
+            rl = roofline_for(r["cfg"], r["B"], dom, st[dom], peaks)
+            rl["kernel"] = dom
+            tk = traffic.get(name, {}).get(dom)
+            if tk is not None:
+                rl["traffic"] = tk
+            per_stage = {s: {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
+                         for s, v in st.items() for rf in [roofline_for(r["cfg"], r["B"], s, v, peaks)]}
+            configs[name] = {"ms_per_layer": round(r["ms"], 5), "tflops_direct_equiv": round(r["tflops"], 2),
+                             "stages": per_stage, "dominant": rl,
+                             "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
+                             "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
+                             "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk")}}
+        out["roofline"] = configs[args.config]["dominant"]
+        out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_sample(cfg, args.cpu_seconds)
+        out["e2e"] = {"value": round(head["e2e_tflops"], 3), "unit": "TFLOP/s",
+                      "h2d_bytes_per_step": head["h2d"], "d2h_bytes_per_step": head["d2h"],
+                      "ms_per_step": round(head["e2e_ms"], 4),
+                      "path": "wino_forward_host (pinned host buffers, H2D + forward + D2H + sync)"}
+        out["gpu_launches"] = head["launches"]
+        out["clocks"] = clocks
+        out["filter_transform_ms"] = configs[args.config]["filter_transform_ms"]
+        out["stages"] = configs[args.config]["stages"]
+        out["configs"] = configs
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_reference(args, world):
+    """The float64 oracle as the reference arm, each step a bounded sample."""
+    import numpy as np
+    from oracle import direct
+    from paper_1611_06565_b200.workloads import CONFIGS, make_inputs
+    cfg = CONFIGS[args.config]
+    x, g = make_inputs(cfg)
+    xn, gn = x.numpy(), g.numpy()
+    per_pt = 2 * cfg.C * cfg.r ** cfg.N
+    n_out = cfg.batch * cfg.K * math.prod(cfg.out_dims)
+    rng = np.random.default_rng(0)
+    npts = max(256, int(1.5e9 / per_pt))          # ~1.5 GFLOP of f64 work per step
+    for _ in range(max(args.warmup, 1)):
+        direct.direct_conv_at(xn, gn, cfg.pad, rng.integers(0, n_out, min(npts, 4096)))
+    times = []
+    for _ in range(args.steps):
+        idx = rng.integers(0, n_out, npts)
+        t0 = time.perf_counter()
+        direct.direct_conv_at(xn, gn, cfg.pad, idx)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = npts * per_pt / (ms * 1e-3) / 1e12
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": round(ms, 3),
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, BASELINE.json distributions; no dataset)",
+           "config": cfg_dict(cfg, cfg.batch, 1, args.scaling),
+           "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": direct.num_threads(),
+                            "kind": "oracle",
+                            "sample": "%d random outputs of %s per step (float64 direct correlation)" % (npts, cfg.name)},
+           "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "ms_per_layer_extrapolated": round(cfg.direct_flops() / (value * 1e12) * 1e3, 1)}
+    print(json.dumps(out))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
