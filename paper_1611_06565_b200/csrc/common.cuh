@@ -38,6 +38,16 @@ struct KGeom {
   int64_t T_s;               // row stride of V and M (>= planned T, multiple of 32)
   int C, K;
   int m;                     // output tile length (runtime copy)
+  // Input-transform slab (xform_in.cu, plan_input_slab): one CTA stages, for
+  // one (b, c) plane, the input needed by tiles [a, a + bt0) along axis 0 and
+  // every tile along axes 1..N-1 (a contiguous run of t), zero padded.
+  int bt0;                   // tiles along axis 0 per CTA
+  int nbox0;                 // ceil(tiles[0] / bt0)
+  int e[kMaxN];              // slab extents for a full box (axis 0: bt0*m + alpha - m)
+  int pitch;                 // padded last-axis extent (multiple of 4 floats)
+  int sst[kMaxN];            // slab element strides (sst[N-1] = 1)
+  int R;                     // tiles per axis-0 slice: prod_{n>=1} tiles[n]
+  int slab_bytes;            // dynamic shared memory of the input kernel
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

@@ -10,8 +10,13 @@ namespace wino {
 enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
 
 bool xform_supported(int N, int alpha, int m, int spec);
-cudaError_t launch_xform(bool input, int N, int alpha, int m, int spec, const float* src, float* dst,
-                         const KGeom& g, const XfParams& xp, cudaStream_t s);
+bool plan_input_slab(KGeom& g, int N, int alpha, int m);
+// a2: x [B][C][in...] -> V [P][C][T_s] for samples [0, B) (g.T = B * Tps)
+cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
+                               const XfParams& xp, int B, cudaStream_t s);
+// a4: M [P][K][T_s] -> y [B][K][out...]
+cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
+                                const XfParams& xp, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s);
 

@@ -282,6 +282,10 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
     sin *= p->in[n]; sout *= p->out[n];
   }
   g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m;
+  if (!plan_input_slab(g, N, a, m)) {
+    delete p;
+    return fail(WINO_ERR_UNSUPPORTED, "input slab of one axis-0 tile exceeds shared memory (inner extents too large)");
+  }
 
   // device buffers
   if (device < 0) {
@@ -303,6 +307,14 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
                 cudaGetErrorString(e));
   }
   p->M = p->V + (size_t)p->P * C * p->T_s;
+  // GEMM padding rows t in [T, T_s) of V are never written: zero them once
+  e = cudaMemset(p->V, 0, p->ws_bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p->ubuf);
+    cudaFree(p->V);
+    delete p;
+    return fail(WINO_ERR_CUDA, "workspace memset failed: %s", cudaGetErrorString(e));
+  }
   if (p->gemm_mode == WINO_GEMM_FFMA) {
     p->U32 = p->ubuf;
   } else {
@@ -363,7 +375,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     ev = &p->ev[4 * (size_t)p->prof_calls];
     CUDA_TRY(cudaEventRecord(ev[0], s));
   }
-  CUDA_TRY(launch_xform(true, p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, s));
+  CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, B, s));
   if (rec) CUDA_TRY(cudaEventRecord(ev[1], s));
   if (p->gemm_mode == WINO_GEMM_FFMA) {
     CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, (int)p->K_s, s));
@@ -371,7 +383,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, s));
   }
   if (rec) CUDA_TRY(cudaEventRecord(ev[2], s));
-  CUDA_TRY(launch_xform(false, p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
+  CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
   if (rec) {
     CUDA_TRY(cudaEventRecord(ev[3], s));
     ++p->prof_calls;
