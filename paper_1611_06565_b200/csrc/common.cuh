@@ -45,6 +45,7 @@ struct KGeom {
   int nbox0;                 // ceil(tiles[0] / bt0)
   int e[kMaxN];              // slab extents for a full box (axis 0: bt0*m + alpha - m)
   int pitch;                 // padded last-axis extent (multiple of 4 floats)
+  int dL;                    // TMA column shift of the slab rows (0 or 3)
   int sst[kMaxN];            // slab element strides (sst[N-1] = 1)
   int R;                     // tiles per axis-0 slice: prod_{n>=1} tiles[n]
   int slab_bytes;            // dynamic shared memory of the input kernel

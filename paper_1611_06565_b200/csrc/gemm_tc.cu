@@ -22,6 +22,7 @@
 #include <cstdio>
 
 #include "kernels.h"
+#include "tma.hpp"
 
 namespace wino {
 namespace tc {
@@ -313,22 +314,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
 // ---------------------------------------------------------------- host side
 cudaError_t tc_set_debug(float* p) { return cudaMemcpyToSymbol(tc::g_dbg, &p, sizeof(p)); }
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn get_encode() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
 
 // 3-D view (inner, c, xi) of a [P][C][inner_s] fp32 array; box {32, kc, 1}.
 static cudaError_t encode3d(CUtensorMap* tm, const float* base, int64_t inner_s, int C, int P, int kc) {

@@ -10,10 +10,12 @@ namespace wino {
 enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
 
 bool xform_supported(int N, int alpha, int m, int spec);
-bool plan_input_slab(KGeom& g, int N, int alpha, int m);
+bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma);
 // a2: x [B][C][in...] -> V [P][C][T_s] for samples [0, B) (g.T = B * Tps)
+// tm: TMA map of x from encode_input_map (NULL = cp.async fallback path)
+bool encode_input_map(CUtensorMap* tm, const float* x, const KGeom& g, int N, int B);
 cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
-                               const XfParams& xp, int B, cudaStream_t s);
+                               const XfParams& xp, const CUtensorMap* tm, int B, cudaStream_t s);
 // a4: M [P][K][T_s] -> y [B][K][out...]
 cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
                                 const XfParams& xp, cudaStream_t s);

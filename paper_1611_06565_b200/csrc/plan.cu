@@ -184,6 +184,11 @@ struct wino_plan_s {
   float *x_dev = nullptr, *y_dev = nullptr;
   bool filter_ready = false;
   TcGemm tg{};
+  CUtensorMap tm_x{};          // input-transform TMA map (cached per x pointer / B)
+  const float* tm_x_ptr = nullptr;
+  int tm_x_B = 0;
+  bool tm_x_ok = false;
+  bool use_tma_in = true;      // env WINO_IN_TMA=0 forces the cp.async path
   bool prof = false;
   int prof_calls = 0;
   std::vector<cudaEvent_t> ev;  // 4 per recorded call
@@ -244,6 +249,7 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? WINO_GEMM_3XTF32 : gemm_mode;
   p->fuse = fuse;
   p->spec = spec;
+  if (const char* ev = getenv("WINO_IN_TMA")) p->use_tma_in = atoi(ev) != 0;
   p->tf = t;
   int64_t Tps = 1;
   for (int n = 0; n < N; ++n) {
@@ -282,7 +288,10 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
     sin *= p->in[n]; sout *= p->out[n];
   }
   g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m;
-  if (!plan_input_slab(g, N, a, m)) {
+  // the TMA slab needs 16-byte strides and the compile-time tables
+  const bool tma_shape = N >= 2 && spec != kSpecRuntime && (p->in[N - 1] % 4) == 0;
+  p->use_tma_in = p->use_tma_in && tma_shape;
+  if (!plan_input_slab(g, N, a, m, p->use_tma_in)) {
     delete p;
     return fail(WINO_ERR_UNSUPPORTED, "input slab of one axis-0 tile exceeds shared memory (inner extents too large)");
   }
@@ -375,7 +384,14 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     ev = &p->ev[4 * (size_t)p->prof_calls];
     CUDA_TRY(cudaEventRecord(ev[0], s));
   }
-  CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, B, s));
+  // TMA map of x, re-encoded when the input pointer or batch changes
+  if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
+    p->tm_x_ok = encode_input_map(&p->tm_x, x, g, p->N, B);
+    p->tm_x_ptr = x;
+    p->tm_x_B = B;
+  }
+  const CUtensorMap* tm = p->use_tma_in && p->tm_x_ok ? &p->tm_x : nullptr;
+  CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, tm, B, s));
   if (rec) CUDA_TRY(cudaEventRecord(ev[1], s));
   if (p->gemm_mode == WINO_GEMM_FFMA) {
     CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, (int)p->K_s, s));

@@ -1,0 +1,302 @@
+// xform_in.cuh -- stage a2, the input-tile (data) transform of the N-D
+// Winograd layer on sm_100a (kernel template; instantiated by
+// xform_in_const.cu for the compile-time tables and xform_in_run.cu for
+// run-time tables):
+//
+//   V_xi[c][t] = (d(b, c, t) x_1 B^T x_2 ... x_N B^T)_xi          (Eq. (4))
+//
+// where d(b, c, t) is the alpha^N window of x starting at t_n*m - P_n, zero
+// outside the input (readings #2, #10).
+//
+// Design: the stage is HBM-bound (x read once, V written
+// once, V = (alpha/m)^N x larger than x), so one CTA owns one (b, c) plane
+// slab -- the input under tiles [a, a+bt0) of axis 0 and all tiles of the
+// other axes, which is a contiguous run of t -- and
+//   1. stages the slab into shared memory: one TMA box load whose
+//      out-of-bounds fill supplies the zero padding (kTma), or coalesced
+//      4-byte cp.async (fallback for shapes that break a TMA rule),
+//   2. runs one work item per (xi_0, tile): the axis-0 combination
+//      h = sum_i B^T[xi_0][i] slab_row(i) (compile-time xi_0, so zero
+//      entries of B^T are skipped), then the remaining N-1 axes as register
+//      line transforms, reading window rows with 64/128-bit shared loads,
+//   3. writes the alpha^(N-1) values V[(xi_0, .)][c][t]; lanes hold
+//      consecutive t, so every warp store is one coalesced 128-byte line.
+//
+// TMA requires the innermost start coordinate to be 16-byte aligned
+// (measured: a start of -1 float faults, -4 works), so the TMA slab starts
+// D = (-P_last) mod 4 columns early and the window reads are shifted by the
+// compile-time D.
+#pragma once
+#include "kernels.h"
+#include "xform_common.cuh"
+
+namespace wino {
+namespace in_detail {
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Read slab columns [Q, END) of a row whose base p is aligned to CAP floats,
+// with the widest aligned vector loads.
+template <int CAP, int Q, int END>
+__device__ __forceinline__ void load_seg(const float* p, float* r) {
+  if constexpr (Q < END) {
+    constexpr int W = (CAP >= 4 && Q % 4 == 0 && Q + 4 <= END) ? 4
+                      : (CAP >= 2 && Q % 2 == 0 && Q + 2 <= END) ? 2 : 1;
+    if constexpr (W == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(p + Q);
+      r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+    } else if constexpr (W == 2) {
+      const float2 v = *reinterpret_cast<const float2*>(p + Q);
+      r[0] = v.x; r[1] = v.y;
+    } else {
+      r[0] = p[Q];
+    }
+    load_seg<CAP, Q + W, END>(p, r + W);
+  }
+}
+
+// A window values of one row: columns [D, D + A) of base p (p aligned to m floats).
+template <int A, int M, int D>
+__device__ __forceinline__ void load_row(const float* p, float* r) {
+  constexpr int cap = M % 4 == 0 ? 4 : M % 2 == 0 ? 2 : 1;
+  load_seg<cap, D, D + A>(p, r);
+}
+
+// One work item: axis-0 output point X0 of one tile whose window starts at
+// slab offset `base` (+ D columns); writes alpha^(N-1) values of V.
+template <int N, int A, int M, class Tab, int D, int X0>
+__device__ __forceinline__ void in_work(const float* __restrict__ S, int base, const KGeom& g,
+                                        const XfParams& xp, float* __restrict__ vout, int64_t pstride) {
+  using Get = BTget<Tab>;
+  if constexpr (N == 1) {
+    float h[A];
+    load_row<A, M, D>(S + base, h);
+    all_axes<A, 1, A, A, Get>(h, xp);
+#pragma unroll
+    for (int j = 0; j < A; ++j) vout[j * pstride] = h[j];
+  } else {
+    constexpr int NL = N - 1;            // axes handled in registers
+    constexpr int P1 = ipow(A, NL);      // values per work item
+    constexpr int ROWS = ipow(A, NL - 1);
+    float h[P1];
+#pragma unroll
+    for (int j = 0; j < P1; ++j) h[j] = 0.f;
+    bool first = true;
+#pragma unroll
+    for (int i0 = 0; i0 < A; ++i0) {
+      if (!Get::nz(xp, X0, i0)) continue;
+      const float bv = Get::v(xp, X0, i0);
+#pragma unroll
+      for (int rw = 0; rw < ROWS; ++rw) {
+        int off = base + i0 * g.sst[0];
+        // row rw enumerates (i_1 .. i_{N-2}) with i_{N-2} fastest
+#pragma unroll
+        for (int ax = 1; ax < N - 1; ++ax) off += ((rw / ipow(A, N - 2 - ax)) % A) * g.sst[ax];
+        float r[A];
+        load_row<A, M, D>(S + off, r);
+#pragma unroll
+        for (int i = 0; i < A; ++i) h[rw * A + i] = first ? bv * r[i] : fmaf(bv, r[i], h[rw * A + i]);
+      }
+      first = false;
+    }
+    all_axes<A, NL, A, A, Get>(h, xp);
+#pragma unroll
+    for (int j = 0; j < P1; ++j) vout[(X0 * P1 + j) * pstride] = h[j];
+  }
+}
+
+template <int N, int A, int M, class Tab, int D, int X0 = 0>
+__device__ __forceinline__ void in_dispatch(int xi0, const float* S, int base, const KGeom& g, const XfParams& xp,
+                                            float* vout, int64_t pstride) {
+  if constexpr (X0 < A) {
+    if (xi0 == X0) in_work<N, A, M, Tab, D, X0>(S, base, g, xp, vout, pstride);
+    else in_dispatch<N, A, M, Tab, D, X0 + 1>(xi0, S, base, g, xp, vout, pstride);
+  }
+}
+
+__device__ __forceinline__ void tma_load_slab(uint32_t dst, const CUtensorMap* tm, const int* co, uint32_t bar,
+                                              int rank) {
+  switch (rank) {
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+          "l"(tm), "r"(co[0]), "r"(co[1]), "r"(co[2]), "r"(bar)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+          "l"(tm), "r"(co[0]), "r"(co[1]), "r"(co[2]), "r"(co[3]), "r"(bar)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+          "l"(tm), "r"(co[0]), "r"(co[1]), "r"(co[2]), "r"(co[3]), "r"(co[4]), "r"(bar)
+          : "memory");
+      break;
+  }
+}
+
+// kTma (N >= 2): slab via one TMA box starting D columns left of -P_last.
+// !kTma: cp.async fallback, D == 0.
+template <int N, int A, int M, class Tab, int D, bool kTma>
+__global__ void __launch_bounds__(256)
+k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
+              const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(128) float S[];
+  __shared__ __align__(8) uint64_t bar;
+  const int box = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
+  const int a0 = box * g.bt0;
+  const int nt0 = min(g.bt0, g.tiles[0] - a0);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
+
+  // ---- 1. slab -> shared memory (zero fill outside the input)
+  if constexpr (kTma) {
+    static_assert(N >= 2, "TMA slab path needs N >= 2");
+    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      int co[5];
+      co[0] = -g.pad[N - 1] - D;
+#pragma unroll
+      for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : 0) - g.pad[ax];
+      co[N] = b * g.C + c;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(g.slab_bytes) : "memory");
+      tma_load_slab(sbase, &tm, co, mb, N + 1);
+    }
+    __syncthreads();
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(mb)
+          : "memory");
+    }
+  } else {
+    static_assert(D == 0, "the cp.async slab path is unshifted");
+    const int e0 = nt0 * M + (A - M);
+    const float* __restrict__ xb = x + ((int64_t)b * g.C + c) * g.in_vol;
+    int rows = N == 1 ? 1 : e0;
+#pragma unroll
+    for (int ax = 1; ax < N - 1; ++ax) rows *= g.e[ax];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    // last axis: extent and global start of the slab row
+    const int eL = N == 1 ? e0 : g.e[N - 1];
+    const int64_t startL = (N == 1 ? (int64_t)a0 * M : 0) - g.pad[N - 1];
+    const int64_t inL = g.in[N - 1];
+    const int cols = N == 1 ? (e0 + 3) / 4 * 4 : g.pitch;
+    for (int row = warp; row < rows; row += nwarps) {
+      // decode row -> slab coordinates (i_0 .. i_{N-2}); global = start + i
+      int rem = row;
+      bool ok = true;
+      int64_t goff = 0;
+      int soff = 0;
+#pragma unroll
+      for (int ax = N - 2; ax >= 0; --ax) {
+        const int ext = ax == 0 ? e0 : g.e[ax];
+        const int i = ax == 0 ? rem : rem % ext;
+        rem = ax == 0 ? 0 : rem / ext;
+        const int64_t p = (ax == 0 ? (int64_t)a0 * M : 0) - g.pad[ax] + i;
+        ok = ok && p >= 0 && p < g.in[ax];
+        goff += p * g.in_stride[ax];
+        soff += i * g.sst[ax];
+      }
+      const float* src = xb + goff + startL;
+      float* drow = S + soff;
+      // columns [lo, hi) are copied, the rest are zero
+      const int lo = ok ? (int)max((int64_t)0, -startL) : cols;
+      const int hi = ok ? (int)min((int64_t)eL, inL - startL) : cols;
+      const uint32_t dst = sbase + 4u * (uint32_t)soff;
+      for (int col = lane; col < cols; col += 32) {
+        if (col >= lo && col < hi) cp_async4(dst + 4u * col, src + col);
+        else drow[col] = 0.f;
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
+
+  // ---- 2./3. work items (xi_0, tile), tile fastest
+  const int ntile = nt0 * g.R;
+  constexpr int NX = N >= 2 ? A : 1;
+  const int64_t pstride = (int64_t)g.C * g.T_s;
+  const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R;
+  float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
+  for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
+    const int xi0 = w / ntile;
+    const int tl = w - xi0 * ntile;
+    // local tile -> slab offset of its window
+    int rem = tl, base = 0;
+#pragma unroll
+    for (int ax = N - 1; ax >= 1; --ax) {
+      const int ti = rem % g.tiles[ax];
+      rem /= g.tiles[ax];
+      base += ti * M * g.sst[ax];
+    }
+    base += rem * M * g.sst[0];
+    in_dispatch<N, A, M, Tab, D>(xi0, S, base, g, xp, vbase + tl, pstride);
+  }
+}
+
+template <class K>
+inline cudaError_t set_smem(K kern, int bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// Launch one (N, alpha, m, table) instantiation.  tm != NULL selects the TMA
+// slab (g.dL is its column shift, 0 or 3); kAllowTma = false compiles only the
+// fallback (run-time tables).
+template <int N, int A, int M, class Tab, bool kAllowTma>
+cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& xp, const CUtensorMap* tm, int B,
+                      cudaStream_t s) {
+  dim3 grid((unsigned)g.nbox0, (unsigned)g.C, (unsigned)B);
+  cudaError_t e;
+  if constexpr (kAllowTma && N >= 2) {
+    if (tm && g.dL == 0) {
+      auto kern = k_input_xform<N, A, M, Tab, 0, true>;
+      if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
+      kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, *tm);
+      return cudaGetLastError();
+    }
+    if (tm && g.dL == 3) {
+      auto kern = k_input_xform<N, A, M, Tab, 3, true>;
+      if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
+      kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, *tm);
+      return cudaGetLastError();
+    }
+  }
+  auto kern = k_input_xform<N, A, M, Tab, 0, false>;
+  if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
+  CUtensorMap dummy{};
+  kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, dummy);
+  return cudaGetLastError();
+}
+
+template <int A, int M, class Tab, bool kAllowTma>
+cudaError_t launch_in_byN(int N, const float* x, float* V, const KGeom& g, const XfParams& xp,
+                          const CUtensorMap* tm, int B, cudaStream_t s) {
+  switch (N) {
+    case 1: return launch_in<1, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+    case 2: return launch_in<2, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+    case 3: return launch_in<3, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+    case 4:
+      if constexpr (ipow(A, 3) <= 64) return launch_in<4, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+      else return cudaErrorNotSupported;
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace in_detail
+
+cudaError_t launch_input_const(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
+                               const XfParams& xp, const CUtensorMap* tm, int B, cudaStream_t s);
+cudaError_t launch_input_run(int N, int alpha, int m, const float* x, float* V, const KGeom& g, const XfParams& xp,
+                             int B, cudaStream_t s);
+
+}  // namespace wino

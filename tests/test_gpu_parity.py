@@ -190,3 +190,16 @@ def test_filter_buffer_roundtrip():
     assert torch.equal(p2.forward(x.cuda()).cpu(), y)
     plan.close()
     p2.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_input_cp_async_fallback_matches_tma(name, monkeypatch):
+    # the TMA slab load and the cp.async fallback (used when a shape breaks a
+    # TMA rule) must produce the same bits
+    cfg = SMALL[name]
+    x, g, y_tma, plan = run(cfg)
+    plan.close()
+    monkeypatch.setenv("WINO_IN_TMA", "0")
+    _, _, y_cp, plan = run(cfg)
+    plan.close()
+    assert torch.equal(y_tma, y_cp)
