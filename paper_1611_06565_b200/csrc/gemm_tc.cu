@@ -20,6 +20,7 @@
 //   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> M[xi][k][t]
 //               (each warp stores 32 consecutive t per column: 128 B lines).
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "tma.hpp"
@@ -29,10 +30,6 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int kThreads = 320;
-
-// Debug dump (dev only; set through tc_set_debug): CTA 0 copies its first
-// smem stage after conversion and the raw accumulator of its first unit.
-__device__ float* g_dbg = nullptr;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -124,26 +121,37 @@ constexpr uint32_t tmem_cols(int bn) {
   return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
 }
 
-template <int BN>
+// Work unit u = (xi, n-block, m-block), m-block fastest.
+// kRes (U-resident): CTA i owns the contiguous unit range [i U / G, (i+1) U / G)
+//   and keeps the whole U_xi n-block (hi and lo, all C) in shared memory,
+//   reloading it only when (xi, n-block) changes; the ring streams V only.
+// !kRes (streaming): units strided by the grid; every ring stage carries the
+//   matching U_hi / U_lo chunk as well (used when the U block is too large).
+template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
-          const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int T, long long T_s,
+          const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
           int C, int K, int kc, int three, int stages) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   const uint32_t sbase = sraw + pad;
+  const int n_chunks = (C + kc - 1) / kc;
   const uint32_t a_bytes = (uint32_t)BM * kc * 4;
-  const uint32_t b_bytes = (uint32_t)BN * kc * 4;
-  const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  const uint32_t bar0 = sbase + stages * stage_bytes;  // 8-byte barriers
+  const uint32_t b_bytes = (uint32_t)BN * kc * 4;  // one chunk of U_hi (or U_lo)
+  const uint32_t stage_bytes = kRes ? 2 * a_bytes : 2 * a_bytes + 2 * b_bytes;
+  const uint32_t bres = sbase + stages * stage_bytes;               // resident U_hi, then U_lo
+  const uint32_t bres_bytes = kRes ? 2u * n_chunks * b_bytes : 0u;
+  const uint32_t bar0 = bres + bres_bytes;                          // 8-byte barriers
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto conv = [&](int s) { return bar0 + 8u * (stages + s); };
   auto empty = [&](int s) { return bar0 + 8u * (2 * stages + s); };
   auto tfull = [&](int a) { return bar0 + 8u * (3 * stages + a); };
   auto tempty = [&](int a) { return bar0 + 8u * (3 * stages + 2 + a); };
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + stages * stage_bytes + 8 * (3 * stages + 4));
+  const uint32_t bfull = bar0 + 8u * (3 * stages + 4);
+  const uint32_t bempty = bar0 + 8u * (3 * stages + 5);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar0 - sbase) + 8 * (3 * stages + 6));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kCols = tmem_cols(BN);
@@ -159,6 +167,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_init(tfull(a), 1);
         mbar_init(tempty(a), 128);
       }
+      mbar_init(bfull, 1);
+      mbar_init(bempty, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -172,34 +182,65 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int n_mblk = (T + BM - 1) / BM;
+  const int n_mblk = (T - t_lo + BM - 1) / BM;
   const int n_nblk = (K + BN - 1) / BN;
-  const int n_chunks = (C + kc - 1) / kc;
   const long long per_xi = (long long)n_nblk * n_mblk;
   const long long total = (long long)P * per_xi;
+  // this CTA's units: [u_beg, u_end) step u_step
+  long long u_beg, u_end, u_step;
+  if constexpr (kRes) {
+    u_beg = total * blockIdx.x / gridDim.x;
+    u_end = total * (blockIdx.x + 1) / gridDim.x;
+    u_step = 1;
+  } else {
+    u_beg = blockIdx.x;
+    u_end = total;
+    u_step = gridDim.x;
+  }
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- TMA producer
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t tx = a_bytes + (three ? 2u : 1u) * b_bytes;
-      for (long long u = blockIdx.x; u < total; u += gridDim.x) {
+      long long cur_pair = -1;
+      int nload = 0;
+      const uint32_t tx = kRes ? a_bytes : a_bytes + (three ? 2u : 1u) * b_bytes;
+      for (long long u = u_beg; u < u_end; u += u_step) {
         const int xi = (int)(u / per_xi);
         const int rr = (int)(u % per_xi);
         const int nb = rr / n_mblk, mb = rr % n_mblk;
+        if constexpr (kRes) {
+          const long long pair = u / n_mblk;
+          if (pair != cur_pair) {
+            if (nload > 0) mbar_wait(bempty, (uint32_t)((nload - 1) & 1));
+            mbar_expect_tx(bfull, (three ? 2u : 1u) * n_chunks * b_bytes);
+            for (int ch = 0; ch < n_chunks; ++ch)
+#pragma unroll
+              for (int gq = 0; gq < BN / 32; ++gq) {
+                tma_load_3d(bres + ch * b_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, bfull);
+                if (three)
+                  tma_load_3d(bres + (n_chunks + ch) * b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
+                              bfull);
+              }
+            cur_pair = pair;
+            ++nload;
+          }
+        }
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(empty(s), ph ^ 1u);
           const uint32_t st = sbase + s * stage_bytes;
           mbar_expect_tx(full(s), tx);
 #pragma unroll
           for (int gq = 0; gq < BM / 32; ++gq)
-            tma_load_3d(st + gq * kc * 128, &tmA, mb * BM + gq * 32, ch * kc, xi, full(s));
+            tma_load_3d(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, full(s));
+          if constexpr (!kRes) {
 #pragma unroll
-          for (int gq = 0; gq < BN / 32; ++gq) {
-            tma_load_3d(st + 2 * a_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, full(s));
-            if (three)
-              tma_load_3d(st + 2 * a_bytes + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
-                          full(s));
+            for (int gq = 0; gq < BN / 32; ++gq) {
+              tma_load_3d(st + 2 * a_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, full(s));
+              if (three)
+                tma_load_3d(st + 2 * a_bytes + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
+                            full(s));
+            }
           }
           if (++s == stages) { s = 0; ph ^= 1u; }
         }
@@ -211,7 +252,18 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const uint32_t lbo = (uint32_t)kc * 128u;
       int s = 0;
       uint32_t ph = 0, acc = 0, aph = 0;
-      for (long long u = blockIdx.x; u < total; u += gridDim.x) {
+      long long cur_pair = -1;
+      int nload = 0;
+      for (long long u = u_beg; u < u_end; u += u_step) {
+        if constexpr (kRes) {
+          const long long pair = u / n_mblk;
+          if (pair != cur_pair) {
+            mbar_wait(bfull, (uint32_t)(nload & 1));
+            tc_fence_after();
+            cur_pair = pair;
+            ++nload;
+          }
+        }
         mbar_wait(tempty(acc), aph ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -219,7 +271,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_wait(conv(s), ph);
           tc_fence_after();
           const uint32_t st = sbase + s * stage_bytes;
-          const uint32_t a_hi = st, a_lo = st + a_bytes, b_hi = st + 2 * a_bytes, b_lo = b_hi + b_bytes;
+          const uint32_t a_hi = st, a_lo = st + a_bytes;
+          const uint32_t b_hi = kRes ? bres + ch * b_bytes : st + 2 * a_bytes;
+          const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
           for (int j = 0; j < kc / 8; ++j) {
             const uint32_t off = (uint32_t)j * 1024u;
             const uint32_t accum = (ch | j) != 0;
@@ -239,13 +293,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_commit(tfull(acc));
         acc ^= 1u;
         if (acc == 0) aph ^= 1u;
+        if constexpr (kRes) {
+          // release the resident U block after its last unit
+          if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
+        }
       }
     }
   } else if (warp < 4) {  // ---------------- converter (128 threads)
     int s = 0;
     uint32_t ph = 0;
     const int n4 = (int)(a_bytes / 16);
-    for (long long u = blockIdx.x; u < total; u += gridDim.x) {
+    for (long long u = u_beg; u < u_end; u += u_step) {
       for (int ch = 0; ch < n_chunks; ++ch) {
         mbar_wait(full(s), ph);
         float4* araw = reinterpret_cast<float4*>(smem + s * stage_bytes);
@@ -262,11 +320,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (g_dbg && blockIdx.x == 0 && u == blockIdx.x && ch == 0) {
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          const float* sp = reinterpret_cast<const float*>(smem + s * stage_bytes);
-          for (uint32_t i = threadIdx.x; i < stage_bytes / 4; i += 128) g_dbg[i] = sp[i];
-        }
         mbar_arrive(conv(s));
         if (++s == stages) { s = 0; ph ^= 1u; }
       }
@@ -274,22 +327,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   } else {  // warps 4-7 ------------------ epilogue
     const int q = warp - 4;
     uint32_t acc = 0, aph = 0;
-    for (long long u = blockIdx.x; u < total; u += gridDim.x) {
+    for (long long u = u_beg; u < u_end; u += u_step) {
       const int xi = (int)(u / per_xi);
       const int rr = (int)(u % per_xi);
       const int nb = rr / n_mblk, mb = rr % n_mblk;
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
-      const int t = mb * BM + q * 32 + lane;
+      const int t = t_lo + mb * BM + q * 32 + lane;
       float* out = Mo + (long long)xi * K * T_s + t;
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         const int k0 = nb * BN + cb * 32;
-        if (g_dbg && blockIdx.x == 0 && u == blockIdx.x) {
-          for (int j = 0; j < 32; ++j) g_dbg[65536 + (q * 32 + lane) * 256 + cb * 32 + j] = __uint_as_float(r[j]);
-        }
         if (t < T) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
@@ -313,8 +363,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 }  // namespace tc
 
 // ---------------------------------------------------------------- host side
-cudaError_t tc_set_debug(float* p) { return cudaMemcpyToSymbol(tc::g_dbg, &p, sizeof(p)); }
-
 // 3-D view (inner, c, xi) of a [P][C][inner_s] fp32 array; box {32, kc, 1}.
 static cudaError_t encode3d(CUtensorMap* tm, const float* base, int64_t inner_s, int C, int P, int kc) {
   EncodeTiledFn enc = get_encode();
@@ -336,13 +384,25 @@ static int pick_bn(int K) {
   return 256;
 }
 
-static size_t tc_smem_bytes(int bn, int kc, int* stages_out) {
-  const size_t stage = 2ull * tc::BM * kc * 4 + 2ull * bn * kc * 4;
-  const size_t budget = 232448 - 1024 - 512;
-  int st = (int)(budget / stage);
+// Shared memory of one launch configuration; resident mode keeps the whole
+// U n-block (hi + lo) beside the V ring.
+static size_t tc_smem_bytes(int bn, int kc, int C, bool res, int* stages_out) {
+  const int n_chunks = (C + kc - 1) / kc;
+  const size_t a = 2ull * tc::BM * kc * 4;
+  const size_t stage = res ? a : a + 2ull * bn * kc * 4;
+  const size_t bres = res ? 2ull * n_chunks * bn * kc * 4 : 0;
+  const size_t fixed = 1024 + 512 + bres;
+  const size_t budget = 232448;
+  int st = budget > fixed ? (int)((budget - fixed) / stage) : 0;
   if (st > 6) st = 6;
   if (stages_out) *stages_out = st;
-  return (size_t)st * stage + 1024 + 512;
+  return (size_t)st * stage + fixed;
+}
+
+template <int BN>
+static cudaError_t set_attr(size_t smem, bool res) {
+  return res ? cudaFuncSetAttribute(tc::k_gemm_tc<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+             : cudaFuncSetAttribute(tc::k_gemm_tc<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P, int64_t T_s,
@@ -354,36 +414,52 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   tg.num_sms = sms;
+  // U-resident when the ring still gets >= 2 stages next to the U block
+  int st = 0;
+  tc_smem_bytes(tg.bn, tg.kc, C, true, &st);
+  tg.resident = st >= 2;
+  if (const char* ev = getenv("WINO_GEMM_RES")) tg.resident = tg.resident && atoi(ev) != 0;
   cudaError_t e;
   if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
-  int st;
-  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, &st);
+  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, C, tg.resident, &st);
+  if (st < 2) return cudaErrorInvalidConfiguration;
   switch (tg.bn) {
-    case 32: e = cudaFuncSetAttribute(tc::k_gemm_tc<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 64: e = cudaFuncSetAttribute(tc::k_gemm_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    case 128: e = cudaFuncSetAttribute(tc::k_gemm_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
-    default: e = cudaFuncSetAttribute(tc::k_gemm_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); break;
+    case 32: e = set_attr<32>(smem, tg.resident); break;
+    case 64: e = set_attr<64>(smem, tg.resident); break;
+    case 128: e = set_attr<128>(smem, tg.resident); break;
+    default: e = set_attr<256>(smem, tg.resident); break;
   }
   if (e != cudaSuccess) return e;
   tg.ready = true;
   return cudaSuccess;
 }
 
-cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K,
+template <int BN>
+static void launch_bn(const TcGemm& tg, int grid, size_t smem, cudaStream_t s, float* Mo, int P, int t_lo, int T,
+                      int64_t T_s, int C, int K, int st) {
+  if (tg.resident)
+    tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C, K,
+                                                             tg.kc, tg.three, st);
+  else
+    tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C, K,
+                                                              tg.kc, tg.three, st);
+}
+
+cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s) {
   if (!tg.ready) return cudaErrorNotReady;
   int st;
-  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, &st);
-  const long long units = (long long)P * ((K + tg.bn - 1) / tg.bn) * ((T + tc::BM - 1) / tc::BM);
+  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, C, tg.resident, &st);
+  const long long units = (long long)P * ((K + tg.bn - 1) / tg.bn) * ((T - t_lo + tc::BM - 1) / tc::BM);
   const int grid = (int)(units < tg.num_sms ? units : tg.num_sms);
   if (grid <= 0) return cudaSuccess;
   switch (tg.bn) {
-    case 32: tc::k_gemm_tc<32><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, (int)T, T_s, C, K, tg.kc, tg.three, st); break;
-    case 64: tc::k_gemm_tc<64><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, (int)T, T_s, C, K, tg.kc, tg.three, st); break;
-    case 128: tc::k_gemm_tc<128><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, (int)T, T_s, C, K, tg.kc, tg.three, st); break;
-    default: tc::k_gemm_tc<256><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, (int)T, T_s, C, K, tg.kc, tg.three, st); break;
+    case 32: launch_bn<32>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
+    case 64: launch_bn<64>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
+    case 128: launch_bn<128>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
+    default: launch_bn<256>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
   }
   return cudaGetLastError();
 }

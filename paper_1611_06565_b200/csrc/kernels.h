@@ -35,12 +35,13 @@ struct TcGemm {
   int kc;             // channels per pipeline stage (multiple of 8, <= 32)
   int three;          // 1: 3xTF32, 0: 1xTF32
   int num_sms;
+  bool resident;      // U block kept in shared memory (see k_gemm_tc)
   bool ready;
 };
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,
                             int64_t T_s, int C, int K_s, int K, int three, int device);
-cudaError_t tc_set_debug(float* p);
-cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K,
+// rows [t_lo, T) of every point (t_lo a multiple of 4)
+cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s);
 
 }  // namespace wino

@@ -396,7 +396,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
   if (p->gemm_mode == WINO_GEMM_FFMA) {
     CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, (int)p->K_s, s));
   } else {
-    CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, s));
+    CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, 0, g.T, p->T_s, p->C, p->K, s));
   }
   if (rec) CUDA_TRY(cudaEventRecord(ev[2], s));
   CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
@@ -499,20 +499,6 @@ wino_status wino_profile_read(wino_plan_t p, double* ms, int* calls) {
   }
   if (ms) for (int s = 0; s < 3; ++s) ms[s] = acc[s];
   if (calls) *calls = p->prof_calls;
-  return WINO_OK;
-}
-
-// Dev-only (not in wino.h): allocate / return the tcgen05 debug dump buffer.
-WINO_API wino_status wino_debug_tc_dump(void** ptr, size_t* bytes) {
-  static float* buf = nullptr;
-  const size_t n = (65536 + 128 * 256) * sizeof(float);
-  if (!buf) {
-    CUDA_TRY(cudaMalloc(&buf, n));
-    CUDA_TRY(cudaMemset(buf, 0, n));
-    CUDA_TRY(tc_set_debug(buf));
-  }
-  *ptr = buf;
-  *bytes = n;
   return WINO_OK;
 }
 

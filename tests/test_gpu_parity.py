@@ -203,3 +203,16 @@ def test_input_cp_async_fallback_matches_tma(name, monkeypatch):
     _, _, y_cp, plan = run(cfg)
     plan.close()
     assert torch.equal(y_tma, y_cp)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_gemm_resident_matches_streaming(name, monkeypatch):
+    # the U-resident GEMM schedule and the streaming one issue the same MMAs
+    # in the same order per output tile: identical bits
+    cfg = SMALL[name]
+    x, g, y_res, plan = run(cfg)
+    plan.close()
+    monkeypatch.setenv("WINO_GEMM_RES", "0")
+    _, _, y_str, plan = run(cfg)
+    plan.close()
+    assert torch.equal(y_res, y_str)
