@@ -6,17 +6,19 @@
 //     V = V_hi + V_lo,  U = U_hi + U_lo  (hi = rna_tf32(x), lo = rna_tf32(x - hi))
 //     M = V_lo U_hi + V_hi U_lo + V_hi U_hi       accumulated in fp32 in TMEM.
 //
-// One persistent, warp-specialised kernel; a work unit is (xi, n-block, m-block)
-// of 128 tiles x BN output channels; units are ordered xi-major so concurrently
-// running CTAs share U_xi in L2.
-//   warp 8      TMA producer: V tile (fp32, 128 x kc) + U_hi/U_lo tiles (BN x kc)
-//               into a `stages`-deep smem ring, MN-major, 128B rows with
-//               32-byte swizzle atoms (SWIZZLE_128B_BASE32B).
-//   warps 0-3   converter: split the V tile in place into V_hi and V_lo (the
-//               tf32 rounding must be explicit: the tensor core truncates).
+// One persistent, warp-specialised kernel (352 threads, 1 CTA per SM); a work
+// unit is (xi, n-block, m-block) of 128 tiles x BN output channels.
+//   warp 8      V producer: TMA of raw V chunks (fp32, 128 t x kc c) into a
+//               deep raw ring (MN-major, 128 B rows, SWIZZLE_128B_BASE32B).
+//   warps 0-3   converter: raw V chunk -> V_hi, V_lo in the 2-stage operand
+//               ring (the tf32 rounding must be explicit: the tensor core
+//               would truncate).
+//   warp 10     U producer: U_hi / U_lo chunks into the operand ring, or the
+//               whole U n-block once into a resident region (kRes).
 //   warp 9      MMA issuer (one thread): 3 x (kc/8) tcgen05.mma.kind::tf32
-//               M=128 N=BN K=8 per stage into a double-buffered TMEM accumulator;
-//               tcgen05.commit frees the smem stage / publishes the accumulator.
+//               M=128 N=BN K=8 per chunk into a double-buffered TMEM
+//               accumulator; tcgen05.commit frees operand stages / publishes
+//               the accumulator.
 //   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> M[xi][k][t]
 //               (each warp stores 32 consecutive t per column: 128 B lines).
 #include <cstdio>
@@ -29,7 +31,7 @@ namespace wino {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -121,47 +123,60 @@ constexpr uint32_t tmem_cols(int bn) {
   return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
 }
 
-// Work unit u = (xi, n-block, m-block), m-block fastest.
-// kRes (U-resident): CTA i owns the contiguous unit range [i U / G, (i+1) U / G)
+// Work unit u = (xi, n-block, m-block), m-block fastest.  Two shared-memory
+// rings decouple HBM latency from the tensor core:
+//   raw ring (R stages):  V chunk [kc c][128 t] fp32, straight from TMA;
+//                         deep, so >= ~50 KB of V loads stay in flight;
+//   op ring  (H stages):  the MMA operands of one chunk: V_hi, V_lo (written
+//                         by the converter warps) and, when U is streamed,
+//                         the U_hi / U_lo chunk (TMA by the B producer).
+// kRes (U-resident): CTA i owns the contiguous unit range [i U/G, (i+1) U/G)
 //   and keeps the whole U_xi n-block (hi and lo, all C) in shared memory,
-//   reloading it only when (xi, n-block) changes; the ring streams V only.
-// !kRes (streaming): units strided by the grid; every ring stage carries the
-//   matching U_hi / U_lo chunk as well (used when the U block is too large).
+//   reloading it when (xi, n-block) changes.  !kRes: U chunks ride in the op
+//   ring.  Warps: 0-3 converter, 4-7 epilogue, 8 V producer, 9 MMA issuer,
+//   10 U producer.
 template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-          int C, int K, int kc, int three, int stages) {
+          int C, int K, int kc, int three, int nraw, int nop) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   const uint32_t sbase = sraw + pad;
   const int n_chunks = (C + kc - 1) / kc;
-  const uint32_t a_bytes = (uint32_t)BM * kc * 4;
-  const uint32_t b_bytes = (uint32_t)BN * kc * 4;  // one chunk of U_hi (or U_lo)
-  const uint32_t stage_bytes = kRes ? 2 * a_bytes : 2 * a_bytes + 2 * b_bytes;
-  const uint32_t bres = sbase + stages * stage_bytes;               // resident U_hi, then U_lo
+  const uint32_t a_bytes = (uint32_t)BM * kc * 4;   // one V chunk (raw, hi or lo)
+  const uint32_t b_bytes = (uint32_t)BN * kc * 4;   // one U chunk (hi or lo)
+  const uint32_t op_bytes = kRes ? 2 * a_bytes : 2 * a_bytes + 2 * b_bytes;
+  const uint32_t raw0 = sbase;
+  const uint32_t op0 = raw0 + nraw * a_bytes;
+  const uint32_t bres = op0 + nop * op_bytes;                       // resident U_hi, then U_lo
   const uint32_t bres_bytes = kRes ? 2u * n_chunks * b_bytes : 0u;
   const uint32_t bar0 = bres + bres_bytes;                          // 8-byte barriers
-  auto full = [&](int s) { return bar0 + 8u * s; };
-  auto conv = [&](int s) { return bar0 + 8u * (stages + s); };
-  auto empty = [&](int s) { return bar0 + 8u * (2 * stages + s); };
-  auto tfull = [&](int a) { return bar0 + 8u * (3 * stages + a); };
-  auto tempty = [&](int a) { return bar0 + 8u * (3 * stages + 2 + a); };
-  const uint32_t bfull = bar0 + 8u * (3 * stages + 4);
-  const uint32_t bempty = bar0 + 8u * (3 * stages + 5);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar0 - sbase) + 8 * (3 * stages + 6));
+  auto rfull = [&](int s) { return bar0 + 8u * s; };
+  auto rempty = [&](int s) { return bar0 + 8u * (nraw + s); };
+  auto ofull = [&](int s) { return bar0 + 8u * (2 * nraw + s); };
+  auto oempty = [&](int s) { return bar0 + 8u * (2 * nraw + nop + s); };
+  const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nop);
+  auto tfull = [&](int a) { return bar1 + 8u * a; };
+  auto tempty = [&](int a) { return bar1 + 8u * (2 + a); };
+  const uint32_t bfull = bar1 + 32u;
+  const uint32_t bempty = bar1 + 40u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar1 - sbase) + 48);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kCols = tmem_cols(BN);
 
   if (warp == 9) {
     if (lane == 0) {
-      for (int s = 0; s < stages; ++s) {
-        mbar_init(full(s), 1);
-        mbar_init(conv(s), 128);
-        mbar_init(empty(s), 1);
+      for (int s = 0; s < nraw; ++s) {
+        mbar_init(rfull(s), 1);
+        mbar_init(rempty(s), 1);
+      }
+      for (int s = 0; s < nop; ++s) {
+        mbar_init(ofull(s), kRes ? 1 : 2);   // converter (+ U producer)
+        mbar_init(oempty(s), 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(tfull(a), 1);
@@ -199,50 +214,63 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 
   if (warp == 8) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- V producer (raw ring)
       int s = 0;
       uint32_t ph = 0;
-      long long cur_pair = -1;
-      int nload = 0;
-      const uint32_t tx = kRes ? a_bytes : a_bytes + (three ? 2u : 1u) * b_bytes;
       for (long long u = u_beg; u < u_end; u += u_step) {
         const int xi = (int)(u / per_xi);
-        const int rr = (int)(u % per_xi);
-        const int nb = rr / n_mblk, mb = rr % n_mblk;
-        if constexpr (kRes) {
-          const long long pair = u / n_mblk;
-          if (pair != cur_pair) {
-            if (nload > 0) mbar_wait(bempty, (uint32_t)((nload - 1) & 1));
-            mbar_expect_tx(bfull, (three ? 2u : 1u) * n_chunks * b_bytes);
-            for (int ch = 0; ch < n_chunks; ++ch)
-#pragma unroll
-              for (int gq = 0; gq < BN / 32; ++gq) {
-                tma_load_3d(bres + ch * b_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, bfull);
-                if (three)
-                  tma_load_3d(bres + (n_chunks + ch) * b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
-                              bfull);
-              }
-            cur_pair = pair;
-            ++nload;
-          }
-        }
+        const int mb = (int)(u % per_xi) % n_mblk;
         for (int ch = 0; ch < n_chunks; ++ch) {
-          mbar_wait(empty(s), ph ^ 1u);
-          const uint32_t st = sbase + s * stage_bytes;
-          mbar_expect_tx(full(s), tx);
+          mbar_wait(rempty(s), ph ^ 1u);
+          const uint32_t st = raw0 + s * a_bytes;
+          mbar_expect_tx(rfull(s), a_bytes);
 #pragma unroll
           for (int gq = 0; gq < BM / 32; ++gq)
-            tma_load_3d(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, full(s));
-          if constexpr (!kRes) {
+            tma_load_3d(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, rfull(s));
+          if (++s == nraw) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ---------------- U producer
+      if constexpr (kRes) {
+        long long cur_pair = -1;
+        int nload = 0;
+        for (long long u = u_beg; u < u_end; ++u) {
+          const long long pair = u / n_mblk;
+          if (pair == cur_pair) continue;
+          const int xi = (int)(u / per_xi);
+          const int nb = (int)(u % per_xi) / n_mblk;
+          if (nload > 0) mbar_wait(bempty, (uint32_t)((nload - 1) & 1));
+          mbar_expect_tx(bfull, (three ? 2u : 1u) * n_chunks * b_bytes);
+          for (int ch = 0; ch < n_chunks; ++ch)
 #pragma unroll
             for (int gq = 0; gq < BN / 32; ++gq) {
-              tma_load_3d(st + 2 * a_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, full(s));
+              tma_load_3d(bres + ch * b_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, bfull);
               if (three)
-                tma_load_3d(st + 2 * a_bytes + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
-                            full(s));
+                tma_load_3d(bres + (n_chunks + ch) * b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
+                            bfull);
             }
+          cur_pair = pair;
+          ++nload;
+        }
+      } else {
+        int s = 0;
+        uint32_t ph = 0;
+        for (long long u = u_beg; u < u_end; u += u_step) {
+          const int xi = (int)(u / per_xi);
+          const int nb = (int)(u % per_xi) / n_mblk;
+          for (int ch = 0; ch < n_chunks; ++ch) {
+            mbar_wait(oempty(s), ph ^ 1u);
+            const uint32_t st = op0 + s * op_bytes + 2 * a_bytes;
+            mbar_expect_tx(ofull(s), (three ? 2u : 1u) * b_bytes);
+#pragma unroll
+            for (int gq = 0; gq < BN / 32; ++gq) {
+              tma_load_3d(st + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, ofull(s));
+              if (three) tma_load_3d(st + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi, ofull(s));
+            }
+            if (++s == nop) { s = 0; ph ^= 1u; }
           }
-          if (++s == stages) { s = 0; ph ^= 1u; }
         }
       }
     }
@@ -268,9 +296,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int ch = 0; ch < n_chunks; ++ch) {
-          mbar_wait(conv(s), ph);
+          mbar_wait(ofull(s), ph);
           tc_fence_after();
-          const uint32_t st = sbase + s * stage_bytes;
+          const uint32_t st = op0 + s * op_bytes;
           const uint32_t a_hi = st, a_lo = st + a_bytes;
           const uint32_t b_hi = kRes ? bres + ch * b_bytes : st + 2 * a_bytes;
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
@@ -287,8 +315,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               tc_mma_tf32(d, dah, dbh, idesc, accum);
             }
           }
-          tc_commit(empty(s));
-          if (++s == stages) { s = 0; ph ^= 1u; }
+          tc_commit(oempty(s));
+          if (++s == nop) { s = 0; ph ^= 1u; }
         }
         tc_commit(tfull(acc));
         acc ^= 1u;
@@ -299,20 +327,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       }
     }
-  } else if (warp < 4) {  // ---------------- converter (128 threads)
-    int s = 0;
-    uint32_t ph = 0;
+  } else if (warp < 4) {  // ---------------- converter (128 threads): raw -> hi, lo
+    int rs = 0, os = 0;
+    uint32_t rph = 0, oph = 0;
     const int n4 = (int)(a_bytes / 16);
     for (long long u = u_beg; u < u_end; u += u_step) {
       for (int ch = 0; ch < n_chunks; ++ch) {
-        mbar_wait(full(s), ph);
-        float4* araw = reinterpret_cast<float4*>(smem + s * stage_bytes);
-        float4* alo = reinterpret_cast<float4*>(smem + s * stage_bytes + a_bytes);
+        mbar_wait(rfull(rs), rph);
+        mbar_wait(oempty(os), oph ^ 1u);
+        const float4* araw = reinterpret_cast<const float4*>(smem + rs * a_bytes);
+        float4* ahi = reinterpret_cast<float4*>(smem + (op0 - sbase) + os * op_bytes);
+        float4* alo = reinterpret_cast<float4*>(smem + (op0 - sbase) + os * op_bytes + a_bytes);
+#pragma unroll 4
         for (int i = threadIdx.x; i < n4; i += 128) {
           const float4 v = araw[i];
           float4 h, l;
           h.x = tf32_rna(v.x); h.y = tf32_rna(v.y); h.z = tf32_rna(v.z); h.w = tf32_rna(v.w);
-          araw[i] = h;
+          ahi[i] = h;
           if (three) {
             l.x = tf32_rna(v.x - h.x); l.y = tf32_rna(v.y - h.y);
             l.z = tf32_rna(v.z - h.z); l.w = tf32_rna(v.w - h.w);
@@ -320,11 +351,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(conv(s));
-        if (++s == stages) { s = 0; ph ^= 1u; }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) {
+          mbar_arrive(rempty(rs));
+          mbar_arrive(ofull(os));
+        }
+        if (++rs == nraw) { rs = 0; rph ^= 1u; }
+        if (++os == nop) { os = 0; oph ^= 1u; }
       }
     }
-  } else {  // warps 4-7 ------------------ epilogue
+  } else if (warp < 8) {  // warps 4-7 ------------------ epilogue
     const int q = warp - 4;
     uint32_t acc = 0, aph = 0;
     for (long long u = u_beg; u < u_end; u += u_step) {
@@ -384,19 +420,26 @@ static int pick_bn(int K) {
   return 256;
 }
 
-// Shared memory of one launch configuration; resident mode keeps the whole
-// U n-block (hi + lo) beside the V ring.
-static size_t tc_smem_bytes(int bn, int kc, int C, bool res, int* stages_out) {
+// Shared-memory plan of one launch: raw ring depth, op ring depth, bytes.
+// Resident mode keeps the whole U n-block (hi + lo) beside the two rings.
+struct TcSmem {
+  int nraw, nop;
+  size_t bytes;
+};
+static TcSmem tc_smem(int bn, int kc, int C, bool res) {
   const int n_chunks = (C + kc - 1) / kc;
-  const size_t a = 2ull * tc::BM * kc * 4;
-  const size_t stage = res ? a : a + 2ull * bn * kc * 4;
+  const size_t a = (size_t)tc::BM * kc * 4;
+  const size_t op = res ? 2 * a : 2 * a + 2ull * bn * kc * 4;
   const size_t bres = res ? 2ull * n_chunks * bn * kc * 4 : 0;
-  const size_t fixed = 1024 + 512 + bres;
+  const size_t fixed = 1024 + 1024 + bres;
   const size_t budget = 232448;
-  int st = budget > fixed ? (int)((budget - fixed) / stage) : 0;
-  if (st > 6) st = 6;
-  if (stages_out) *stages_out = st;
-  return (size_t)st * stage + fixed;
+  TcSmem t{0, 2, 0};
+  if (fixed + 2 * op + a > budget) return t;
+  int nraw = (int)((budget - fixed - 2 * op) / a);
+  if (nraw > 8) nraw = 8;
+  t.nraw = nraw;
+  t.bytes = fixed + 2 * op + nraw * a;
+  return t;
 }
 
 template <int BN>
@@ -414,17 +457,16 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   tg.num_sms = sms;
-  // U-resident when the ring still gets >= 2 stages next to the U block
-  int st = 0;
-  tc_smem_bytes(tg.bn, tg.kc, C, true, &st);
-  tg.resident = st >= 2;
+  // U-resident when the raw ring still gets >= 4 stages next to the U block
+  tg.resident = tc_smem(tg.bn, tg.kc, C, true).nraw >= 4;
   if (const char* ev = getenv("WINO_GEMM_RES")) tg.resident = tg.resident && atoi(ev) != 0;
   cudaError_t e;
   if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
-  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, C, tg.resident, &st);
-  if (st < 2) return cudaErrorInvalidConfiguration;
+  const TcSmem sm = tc_smem(tg.bn, tg.kc, C, tg.resident);
+  if (sm.nraw < 1) return cudaErrorInvalidConfiguration;
+  const size_t smem = sm.bytes;
   switch (tg.bn) {
     case 32: e = set_attr<32>(smem, tg.resident); break;
     case 64: e = set_attr<64>(smem, tg.resident); break;
@@ -437,29 +479,28 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
 }
 
 template <int BN>
-static void launch_bn(const TcGemm& tg, int grid, size_t smem, cudaStream_t s, float* Mo, int P, int t_lo, int T,
-                      int64_t T_s, int C, int K, int st) {
+static void launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P, int t_lo,
+                      int T, int64_t T_s, int C, int K) {
   if (tg.resident)
-    tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C, K,
-                                                             tg.kc, tg.three, st);
+    tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
+                                                                 K, tg.kc, tg.three, sm.nraw, sm.nop);
   else
-    tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, smem, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C, K,
-                                                              tg.kc, tg.three, st);
+    tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
+                                                                  K, tg.kc, tg.three, sm.nraw, sm.nop);
 }
 
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s) {
   if (!tg.ready) return cudaErrorNotReady;
-  int st;
-  const size_t smem = tc_smem_bytes(tg.bn, tg.kc, C, tg.resident, &st);
+  const TcSmem sm = tc_smem(tg.bn, tg.kc, C, tg.resident);
   const long long units = (long long)P * ((K + tg.bn - 1) / tg.bn) * ((T - t_lo + tc::BM - 1) / tc::BM);
   const int grid = (int)(units < tg.num_sms ? units : tg.num_sms);
   if (grid <= 0) return cudaSuccess;
   switch (tg.bn) {
-    case 32: launch_bn<32>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
-    case 64: launch_bn<64>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
-    case 128: launch_bn<128>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
-    default: launch_bn<256>(tg, grid, smem, s, Mo, P, (int)t_lo, (int)T, T_s, C, K, st); break;
+    case 32: launch_bn<32>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
+    case 64: launch_bn<64>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
+    case 128: launch_bn<128>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
+    default: launch_bn<256>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
   }
   return cudaGetLastError();
 }
