@@ -84,11 +84,13 @@ struct RunTab {
   __device__ static __forceinline__ float at(const XfParams& p, int x, int i) { return p.AT[x][i]; }
 };
 
-// tf32 round-to-nearest (ties away) of an fp32 value, result as fp32 container.
+// tf32 round-to-nearest, ties away from zero (= cvt.rna.tf32.f32) of a finite
+// fp32 value, result as an fp32 container with the low 13 bits clear.  On the
+// sign-magnitude bit pattern, adding half an ulp of tf32 (0x1000) and
+// truncating rounds the magnitude half-up; two integer ops instead of the
+// NaN/Inf-guarded cvt sequence.
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 }  // namespace wino

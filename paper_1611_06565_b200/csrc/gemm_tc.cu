@@ -299,21 +299,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_wait(ofull(s), ph);
           tc_fence_after();
           const uint32_t st = op0 + s * op_bytes;
-          const uint32_t a_hi = st, a_lo = st + a_bytes;
           const uint32_t b_hi = kRes ? bres + ch * b_bytes : st + 2 * a_bytes;
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
+          // descriptors of k-step 0; k-step j is +j*1024 B = +64 in the address field
+          uint64_t dah = sdesc(st, lbo, 512u), dal = sdesc(st + a_bytes, lbo, 512u);
+          uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
           for (int j = 0; j < kc / 8; ++j) {
-            const uint32_t off = (uint32_t)j * 1024u;
             const uint32_t accum = (ch | j) != 0;
-            const uint64_t dah = sdesc(a_hi + off, lbo, 512u);
-            const uint64_t dbh = sdesc(b_hi + off, lbo, 512u);
             if (three) {
-              tc_mma_tf32(d, sdesc(a_lo + off, lbo, 512u), dbh, idesc, accum);
-              tc_mma_tf32(d, dah, sdesc(b_lo + off, lbo, 512u), idesc, 1u);
+              tc_mma_tf32(d, dal, dbh, idesc, accum);
+              tc_mma_tf32(d, dah, dbl, idesc, 1u);
               tc_mma_tf32(d, dah, dbh, idesc, 1u);
             } else {
               tc_mma_tf32(d, dah, dbh, idesc, accum);
             }
+            dah += 64; dal += 64; dbh += 64; dbl += 64;
           }
           tc_commit(oempty(s));
           if (++s == nop) { s = 0; ph ^= 1u; }
@@ -370,16 +370,29 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
       const int t = t_lo + mb * BM + q * 32 + lane;
-      float* out = Mo + (long long)xi * K * T_s + t;
+      // M[xi][k][t]: this lane's column t, rows k = nb*BN + j (stride T_s)
+      float* out = Mo + ((long long)xi * K + (long long)nb * BN) * T_s + t;
+      const bool full_n = (nb + 1) * BN <= K;
 #pragma unroll 1
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
-        const int k0 = nb * BN + cb * 32;
         if (t < T) {
+          float* p = out + (long long)cb * 32 * T_s;
+          if (full_n) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (k0 + j < K) out[(long long)(k0 + j) * T_s] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j) {
+              __stcs(p, __uint_as_float(r[j]));
+              p += T_s;
+            }
+          } else {
+            const int kr = K - nb * BN - cb * 32;  // valid rows in this 32-block
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < kr) __stcs(p, __uint_as_float(r[j]));
+              p += T_s;
+            }
+          }
         }
       }
       tc_fence_before();
