@@ -50,6 +50,7 @@ def parse_args():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--extra", default="c3,c4,c5", help="comma list of further configs ('' for none)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--fuse", type=int, default=0, help="plan fuse bitmask (4 = L2-chunked a2->a3->a4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
     return ap.parse_args()
@@ -175,7 +176,7 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
             B = hi - lo
             xf, g = make_inputs(cfg, seed=0)
             x = xf[lo:hi].contiguous()
-        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding, device=local)
+        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding, device=local, fuse=args.fuse)
         stream = torch.cuda.current_stream(dev)
         # a1 once per weight set on rank 0, U broadcast over NCCL to the others
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -271,13 +272,14 @@ def cpu_baseline_sample(cfg, seconds):
             "ms_per_layer_extrapolated": round(cfg.direct_flops() / (npts2 * per_pt / dt) * 1e3, 1)}
 
 
-def cfg_dict(cfg, B, world, scaling):
+def cfg_dict(cfg, B, world, scaling, fuse=0):
     return {"workload": "%s: %s" % (cfg.name, cfg.desc), "model": "N-D Winograd conv layer (synthetic)",
             "N": cfg.N, "dims": list(cfg.dims), "C": cfg.C, "K": cfg.K, "kernel": cfg.r, "pad": cfg.pad,
             "F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "per_gpu_batch": B,
             "global_batch": B * world if scaling == "weak" else cfg.batch, "seq_len": None,
             "parallelism": "dp%d (batch shards, U broadcast once)" % world,
             "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate)",
+            "pipeline": "L2-chunked a2->a3->a4" if fuse & 4 else "three kernels, V/M via HBM",
             "l2": "flushed: 256 MiB memset between timed steps, outside the per-step events"}
 
 
@@ -315,7 +317,7 @@ def main():
                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(head["ms"], 5),
                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded, BASELINE.json distributions; no dataset)",
-               "config": cfg_dict(cfg, head["B"], world, args.scaling)}
+               "config": cfg_dict(cfg, head["B"], world, args.scaling, args.fuse)}
         configs = {}
         for name, r in res.items():
             st = r["stages_ms"]
@@ -331,7 +333,8 @@ def main():
                              "stages": per_stage, "dominant": rl,
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
-                             "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk")}}
+                             "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
+                                                                 "chunk_slabs")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
         if world == 1 and not args.no_cpu_baseline:

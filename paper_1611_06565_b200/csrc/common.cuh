@@ -34,8 +34,11 @@ struct KGeom {
   int pad[kMaxN];
   int64_t in_vol, out_vol;   // per (b, c) / (b, k) plane
   int64_t Tps;               // tiles per sample
-  int64_t T;                 // tiles of this call (B * Tps)
-  int64_t T_s;               // row stride of V and M (>= planned T, multiple of 32)
+  int64_t T;                 // end of the tile range of this launch (B * Tps unchunked)
+  int64_t T_s;               // row stride of V and M (multiple of 128)
+  int64_t t_beg;             // first tile of this launch (output transform)
+  int64_t t0;                // V / M row of tile t is t - t0 (L2-chunked buffers)
+  int64_t s_beg;             // first input slab (b * nbox0 + box) of this launch
   int C, K;
   int m;                     // output tile length (runtime copy)
   // Input-transform slab (xform_in.cu, plan_input_slab): one CTA stages, for

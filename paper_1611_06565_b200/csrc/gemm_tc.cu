@@ -139,7 +139,7 @@ template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-          int C, int K, int kc, int three, int nraw, int nop) {
+          int C, int K, int kc, int three, int nraw, int nop, int nbr) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
@@ -148,17 +148,21 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int n_chunks = (C + kc - 1) / kc;
   const uint32_t a_bytes = (uint32_t)BM * kc * 4;   // one V chunk (raw, hi or lo)
   const uint32_t b_bytes = (uint32_t)BN * kc * 4;   // one U chunk (hi or lo)
-  const uint32_t op_bytes = kRes ? 2 * a_bytes : 2 * a_bytes + 2 * b_bytes;
+  const uint32_t op_bytes = 2 * a_bytes;
   const uint32_t raw0 = sbase;
   const uint32_t op0 = raw0 + nraw * a_bytes;
-  const uint32_t bres = op0 + nop * op_bytes;                       // resident U_hi, then U_lo
-  const uint32_t bres_bytes = kRes ? 2u * n_chunks * b_bytes : 0u;
+  // U: the resident block (hi chunks then lo chunks), or a ring of nbr
+  // stages each holding one chunk's U_hi and U_lo
+  const uint32_t bres = op0 + nop * op_bytes;
+  const uint32_t bres_bytes = kRes ? 2u * n_chunks * b_bytes : 2u * nbr * b_bytes;
   const uint32_t bar0 = bres + bres_bytes;                          // 8-byte barriers
   auto rfull = [&](int s) { return bar0 + 8u * s; };
   auto rempty = [&](int s) { return bar0 + 8u * (nraw + s); };
   auto ofull = [&](int s) { return bar0 + 8u * (2 * nraw + s); };
   auto oempty = [&](int s) { return bar0 + 8u * (2 * nraw + nop + s); };
-  const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nop);
+  auto ufull = [&](int s) { return bar0 + 8u * (2 * nraw + 2 * nop + s); };
+  auto uempty = [&](int s) { return bar0 + 8u * (2 * nraw + 2 * nop + nbr + s); };
+  const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nop + 2 * nbr);
   auto tfull = [&](int a) { return bar1 + 8u * a; };
   auto tempty = [&](int a) { return bar1 + 8u * (2 + a); };
   const uint32_t bfull = bar1 + 32u;
@@ -175,8 +179,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_init(rempty(s), 1);
       }
       for (int s = 0; s < nop; ++s) {
-        mbar_init(ofull(s), kRes ? 1 : 2);   // converter (+ U producer)
+        mbar_init(ofull(s), 1);
         mbar_init(oempty(s), 1);
+      }
+      for (int s = 0; s < nbr; ++s) {
+        mbar_init(ufull(s), 1);
+        mbar_init(uempty(s), 1);
       }
       for (int a = 0; a < 2; ++a) {
         mbar_init(tfull(a), 1);
@@ -261,15 +269,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const int xi = (int)(u / per_xi);
           const int nb = (int)(u % per_xi) / n_mblk;
           for (int ch = 0; ch < n_chunks; ++ch) {
-            mbar_wait(oempty(s), ph ^ 1u);
-            const uint32_t st = op0 + s * op_bytes + 2 * a_bytes;
-            mbar_expect_tx(ofull(s), (three ? 2u : 1u) * b_bytes);
+            mbar_wait(uempty(s), ph ^ 1u);
+            const uint32_t st = bres + s * 2 * b_bytes;
+            mbar_expect_tx(ufull(s), (three ? 2u : 1u) * b_bytes);
 #pragma unroll
             for (int gq = 0; gq < BN / 32; ++gq) {
-              tma_load_3d(st + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, ofull(s));
-              if (three) tma_load_3d(st + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi, ofull(s));
+              tma_load_3d(st + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, ufull(s));
+              if (three) tma_load_3d(st + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi, ufull(s));
             }
-            if (++s == nop) { s = 0; ph ^= 1u; }
+            if (++s == nbr) { s = 0; ph ^= 1u; }
           }
         }
       }
@@ -278,8 +286,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (lane == 0) {  // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_tf32<BN>();
       const uint32_t lbo = (uint32_t)kc * 128u;
-      int s = 0;
-      uint32_t ph = 0, acc = 0, aph = 0;
+      int s = 0, us = 0;
+      uint32_t ph = 0, uph = 0, acc = 0, aph = 0;
       long long cur_pair = -1;
       int nload = 0;
       for (long long u = u_beg; u < u_end; u += u_step) {
@@ -297,9 +305,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint32_t d = tmem_base + acc * BN;
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(ofull(s), ph);
+          if constexpr (!kRes) mbar_wait(ufull(us), uph);
           tc_fence_after();
           const uint32_t st = op0 + s * op_bytes;
-          const uint32_t b_hi = kRes ? bres + ch * b_bytes : st + 2 * a_bytes;
+          const uint32_t b_hi = kRes ? bres + ch * b_bytes : bres + us * 2 * b_bytes;
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
           // descriptors of k-step 0; k-step j is +j*1024 B = +64 in the address field
           uint64_t dah = sdesc(st, lbo, 512u), dal = sdesc(st + a_bytes, lbo, 512u);
@@ -317,6 +326,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
           tc_commit(oempty(s));
           if (++s == nop) { s = 0; ph ^= 1u; }
+          if constexpr (!kRes) {
+            tc_commit(uempty(us));
+            if (++us == nbr) { us = 0; uph ^= 1u; }
+          }
         }
         tc_commit(tfull(acc));
         acc ^= 1u;
@@ -436,22 +449,36 @@ static int pick_bn(int K) {
 // Shared-memory plan of one launch: raw ring depth, op ring depth, bytes.
 // Resident mode keeps the whole U n-block (hi + lo) beside the two rings.
 struct TcSmem {
-  int nraw, nop;
+  int nraw, nop, nbr;
   size_t bytes;
 };
+// Rings: raw V (nraw x 128*kc*4), operands V_hi/V_lo (nop = 2), and U either
+// resident (all chunks) or a ring of nbr chunk stages (U_hi + U_lo).  Depth
+// goes first to U (its L2 latency must hide behind <= nbr chunk MMAs), then
+// to the raw V ring.
 static TcSmem tc_smem(int bn, int kc, int C, bool res) {
   const int n_chunks = (C + kc - 1) / kc;
   const size_t a = (size_t)tc::BM * kc * 4;
-  const size_t op = res ? 2 * a : 2 * a + 2ull * bn * kc * 4;
-  const size_t bres = res ? 2ull * n_chunks * bn * kc * 4 : 0;
-  const size_t fixed = 1024 + 1024 + bres;
+  const size_t b2 = 2ull * bn * kc * 4;
+  const size_t fixed = 1024 + 1024;
   const size_t budget = 232448;
-  TcSmem t{0, 2, 0};
-  if (fixed + 2 * op + a > budget) return t;
-  int nraw = (int)((budget - fixed - 2 * op) / a);
+  TcSmem t{0, 2, 0, 0};
+  size_t left = budget - fixed - 2 * (2 * a);
+  if (res) {
+    const size_t bres = (size_t)n_chunks * b2;
+    if (bres + a > left) return t;
+    left -= bres;
+  } else {
+    int nbr = 3;
+    while (nbr > 1 && nbr * b2 + 2 * a > left) --nbr;
+    if (nbr * b2 + a > left) return t;
+    t.nbr = nbr;
+    left -= nbr * b2;
+  }
+  int nraw = (int)(left / a);
   if (nraw > 8) nraw = 8;
   t.nraw = nraw;
-  t.bytes = fixed + 2 * op + nraw * a;
+  t.bytes = budget - (left - nraw * a);
   return t;
 }
 
@@ -496,10 +523,10 @@ static void launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t
                       int T, int64_t T_s, int C, int K) {
   if (tg.resident)
     tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
-                                                                 K, tg.kc, tg.three, sm.nraw, sm.nop);
+                                                                 K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
   else
     tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
-                                                                  K, tg.kc, tg.three, sm.nraw, sm.nop);
+                                                                  K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
 }
 
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,

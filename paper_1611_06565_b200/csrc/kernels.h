@@ -11,12 +11,13 @@ enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
 
 bool xform_supported(int N, int alpha, int m, int spec);
 bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma);
-// a2: x [B][C][in...] -> V [P][C][T_s] for samples [0, B) (g.T = B * Tps)
+// a2: x [B][C][in...] -> V [P][C][T_s], input slabs [g.s_beg, g.s_beg + nslab)
+// (slab = b * nbox0 + box; V row = t - g.t0)
 // tm: TMA map of x from encode_input_map (NULL = cp.async fallback path)
 bool encode_input_map(CUtensorMap* tm, const float* x, const KGeom& g, int N, int B);
 cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
-                               const XfParams& xp, const CUtensorMap* tm, int B, cudaStream_t s);
-// a4: M [P][K][T_s] -> y [B][K][out...]
+                               const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
+// a4: M [P][K][T_s] -> y [B][K][out...] for tiles [g.t_beg, g.T) (M row = t - g.t0)
 cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
                                 const XfParams& xp, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,

@@ -189,11 +189,14 @@ struct wino_plan_s {
   int tm_x_B = 0;
   bool tm_x_ok = false;
   bool use_tma_in = true;      // env WINO_IN_TMA=0 forces the cp.async path
+  // L2-chunked pipeline (fuse & WINO_FUSE_L2_CHUNK): V and M hold one chunk
+  // of chunk_slabs input slabs (rows t - t_lo), sized to stay L2-resident
+  bool chunked = false;
+  int64_t chunk_slabs = 0;
   bool prof = false;
   int prof_calls = 0;
-  std::vector<cudaEvent_t> ev;  // 4 per recorded call
-  double prof_ms[3] = {0, 0, 0};
-  int prof_read = 0;
+  std::vector<cudaEvent_t> ev;  // pool; prof_stage[i] tags pair (2i, 2i+1)
+  std::vector<int> prof_stage;
 };
 
 extern "C" {
@@ -235,7 +238,7 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   if (!dims) return fail(WINO_ERR_ARG, "dims is NULL");
   if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
   if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
-  if (fuse != 0) return fail(WINO_ERR_UNSUPPORTED, "fuse bitmask %d not implemented in this build", fuse);
+  if (fuse & ~WINO_FUSE_L2_CHUNK) return fail(WINO_ERR_UNSUPPORTED, "fuse bitmask %d not implemented in this build", fuse);
   Transforms t;
   int spec;
   wino_status st = synth_checked(m, r, points, t, spec);
@@ -294,6 +297,23 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   if (!plan_input_slab(g, N, a, m, p->use_tma_in)) {
     delete p;
     return fail(WINO_ERR_UNSUPPORTED, "input slab of one axis-0 tile exceeds shared memory (inner extents too large)");
+  }
+
+  // L2 chunking: chunk_slabs input slabs per chunk, V + M of a chunk near
+  // WINO_CHUNK_MB (default 48 MB, under the 126 MB L2 with x / y traffic)
+  if (fuse & WINO_FUSE_L2_CHUNK) {
+    double mb = 48.0;
+    if (const char* ev = getenv("WINO_CHUNK_MB")) mb = atof(ev);
+    const double slab_bytes = (double)g.bt0 * g.R * p->P * (C + K) * 4.0;
+    int64_t cs = (int64_t)(mb * 1048576.0 / slab_bytes);
+    const int64_t nslab = (int64_t)batch * g.nbox0;
+    if (cs < 1) cs = 1;
+    if (cs < nslab) {
+      p->chunked = true;
+      p->chunk_slabs = cs;
+      p->T_s = ((int64_t)cs * g.bt0 * g.R + 127) / 128 * 128;
+      g.T_s = p->T_s;
+    }
   }
 
   // device buffers
@@ -369,21 +389,38 @@ wino_status wino_filter_transform(wino_plan_t p, const float* g, wino_stream_t s
   return WINO_OK;
 }
 
+// First tile of input slab s (flattened b * nbox0 + box).
+static int64_t slab_tile(const KGeom& g, int64_t s) {
+  const int64_t b = s / g.nbox0, box = s % g.nbox0;
+  const int64_t a0 = box * g.bt0 < g.tiles[0] ? box * g.bt0 : g.tiles[0];
+  return b * g.Tps + a0 * g.R;
+}
+
+// Stage timing (wino_profile_*): a start/end event pair around one launch.
+struct ProfScope {
+  wino_plan_t p;
+  cudaStream_t s;
+  int stage;
+  cudaEvent_t b = nullptr, e = nullptr;
+  cudaError_t begin() {
+    const size_t i = p->prof_stage.size();
+    while (p->ev.size() < 2 * (i + 1)) {
+      cudaEvent_t ev;
+      cudaError_t r = cudaEventCreate(&ev);
+      if (r != cudaSuccess) return r;
+      p->ev.push_back(ev);
+    }
+    b = p->ev[2 * i];
+    e = p->ev[2 * i + 1];
+    p->prof_stage.push_back(stage);
+    return cudaEventRecord(b, s);
+  }
+  cudaError_t end() { return cudaEventRecord(e, s); }
+};
+
 static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, cudaStream_t s) {
   KGeom g = p->geom;
-  g.T = (int64_t)B * p->Tps;
   const bool rec = p->prof && p->prof_calls < kMaxProf;
-  cudaEvent_t* ev = nullptr;
-  if (rec) {
-    const size_t need = 4 * (size_t)(p->prof_calls + 1);
-    while (p->ev.size() < need) {
-      cudaEvent_t e;
-      CUDA_TRY(cudaEventCreate(&e));
-      p->ev.push_back(e);
-    }
-    ev = &p->ev[4 * (size_t)p->prof_calls];
-    CUDA_TRY(cudaEventRecord(ev[0], s));
-  }
   // TMA map of x, re-encoded when the input pointer or batch changes
   if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
     p->tm_x_ok = encode_input_map(&p->tm_x, x, g, p->N, B);
@@ -391,19 +428,33 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     p->tm_x_B = B;
   }
   const CUtensorMap* tm = p->use_tma_in && p->tm_x_ok ? &p->tm_x : nullptr;
-  CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, tm, B, s));
-  if (rec) CUDA_TRY(cudaEventRecord(ev[1], s));
-  if (p->gemm_mode == WINO_GEMM_FFMA) {
-    CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, g.T, p->T_s, p->C, p->K, (int)p->K_s, s));
-  } else {
-    CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, 0, g.T, p->T_s, p->C, p->K, s));
+  const int64_t nslab = (int64_t)B * g.nbox0;
+  const int64_t step = p->chunked ? p->chunk_slabs : nslab;
+  for (int64_t s0 = 0; s0 < nslab; s0 += step) {
+    const int64_t s1 = s0 + step < nslab ? s0 + step : nslab;
+    const int64_t t_lo = slab_tile(g, s0), t_hi = slab_tile(g, s1);
+    g.s_beg = s0;
+    g.t0 = p->chunked ? t_lo : 0;
+    g.t_beg = t_lo;
+    g.T = t_hi;
+    ProfScope ps{p, s, 0};
+    if (rec) CUDA_TRY(ps.begin());
+    CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, tm, (int)(s1 - s0), s));
+    if (rec) CUDA_TRY(ps.end());
+    ProfScope pg{p, s, 1};
+    if (rec) CUDA_TRY(pg.begin());
+    if (p->gemm_mode == WINO_GEMM_FFMA) {
+      CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, t_hi - g.t0, p->T_s, p->C, p->K, (int)p->K_s, s));
+    } else {
+      CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, t_lo - g.t0, t_hi - g.t0, p->T_s, p->C, p->K, s));
+    }
+    if (rec) CUDA_TRY(pg.end());
+    ProfScope po{p, s, 2};
+    if (rec) CUDA_TRY(po.begin());
+    CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
+    if (rec) CUDA_TRY(po.end());
   }
-  if (rec) CUDA_TRY(cudaEventRecord(ev[2], s));
-  CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
-  if (rec) {
-    CUDA_TRY(cudaEventRecord(ev[3], s));
-    ++p->prof_calls;
-  }
+  if (rec) ++p->prof_calls;
   return WINO_OK;
 }
 
@@ -452,7 +503,7 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
   const int64_t v[16] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
-                         p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->spec};
+                         p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }
@@ -481,6 +532,7 @@ wino_status wino_profile_enable(wino_plan_t p, int enable) {
   if (!p) return fail(WINO_ERR_ARG, "NULL plan");
   p->prof = enable != 0;
   p->prof_calls = 0;
+  p->prof_stage.clear();
   return WINO_OK;
 }
 
@@ -488,14 +540,11 @@ wino_status wino_profile_read(wino_plan_t p, double* ms, int* calls) {
   if (!p) return fail(WINO_ERR_ARG, "NULL plan");
   DeviceGuard guard(p->device);
   double acc[3] = {0, 0, 0};
-  for (int c = 0; c < p->prof_calls; ++c) {
-    cudaEvent_t* e = &p->ev[4 * (size_t)c];
-    CUDA_TRY(cudaEventSynchronize(e[3]));
-    for (int s = 0; s < 3; ++s) {
-      float t = 0.f;
-      CUDA_TRY(cudaEventElapsedTime(&t, e[s], e[s + 1]));
-      acc[s] += t;
-    }
+  for (size_t i = 0; i < p->prof_stage.size(); ++i) {
+    CUDA_TRY(cudaEventSynchronize(p->ev[2 * i + 1]));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, p->ev[2 * i], p->ev[2 * i + 1]));
+    acc[p->prof_stage[i]] += t;
   }
   if (ms) for (int s = 0; s < 3; ++s) ms[s] = acc[s];
   if (calls) *calls = p->prof_calls;

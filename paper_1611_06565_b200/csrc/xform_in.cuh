@@ -148,7 +148,8 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
               const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) float S[];
   __shared__ __align__(8) uint64_t bar;
-  const int box = blockIdx.x, c = blockIdx.y, b = blockIdx.z;
+  const int64_t slab = g.s_beg + blockIdx.x;
+  const int b = (int)(slab / g.nbox0), box = (int)(slab - (int64_t)b * g.nbox0), c = blockIdx.y;
   const int a0 = box * g.bt0;
   const int nt0 = min(g.bt0, g.tiles[0] - a0);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
@@ -225,7 +226,7 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   const int ntile = nt0 * g.R;
   constexpr int NX = N >= 2 ? A : 1;
   const int64_t pstride = (int64_t)g.C * g.T_s;
-  const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R;
+  const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;  // V row of the slab's first tile
   float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
   for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
     const int xi0 = w / ntile;
@@ -252,10 +253,11 @@ inline cudaError_t set_smem(K kern, int bytes) {
 // Launch one (N, alpha, m, table) instantiation.  tm != NULL selects the TMA
 // slab (g.dL is its column shift, 0 or 3); kAllowTma = false compiles only the
 // fallback (run-time tables).
+// Slabs [g.s_beg, g.s_beg + nslab) of the flattened (b, box) order.
 template <int N, int A, int M, class Tab, bool kAllowTma>
-cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& xp, const CUtensorMap* tm, int B,
+cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& xp, const CUtensorMap* tm, int nslab,
                       cudaStream_t s) {
-  dim3 grid((unsigned)g.nbox0, (unsigned)g.C, (unsigned)B);
+  dim3 grid((unsigned)nslab, (unsigned)g.C);
   cudaError_t e;
   if constexpr (kAllowTma && N >= 2) {
     if (tm && g.dL == 0) {
@@ -280,13 +282,13 @@ cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& 
 
 template <int A, int M, class Tab, bool kAllowTma>
 cudaError_t launch_in_byN(int N, const float* x, float* V, const KGeom& g, const XfParams& xp,
-                          const CUtensorMap* tm, int B, cudaStream_t s) {
+                          const CUtensorMap* tm, int nslab, cudaStream_t s) {
   switch (N) {
-    case 1: return launch_in<1, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
-    case 2: return launch_in<2, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
-    case 3: return launch_in<3, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+    case 1: return launch_in<1, A, M, Tab, kAllowTma>(x, V, g, xp, tm, nslab, s);
+    case 2: return launch_in<2, A, M, Tab, kAllowTma>(x, V, g, xp, tm, nslab, s);
+    case 3: return launch_in<3, A, M, Tab, kAllowTma>(x, V, g, xp, tm, nslab, s);
     case 4:
-      if constexpr (ipow(A, 3) <= 64) return launch_in<4, A, M, Tab, kAllowTma>(x, V, g, xp, tm, B, s);
+      if constexpr (ipow(A, 3) <= 64) return launch_in<4, A, M, Tab, kAllowTma>(x, V, g, xp, tm, nslab, s);
       else return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
@@ -295,8 +297,8 @@ cudaError_t launch_in_byN(int N, const float* x, float* V, const KGeom& g, const
 }  // namespace in_detail
 
 cudaError_t launch_input_const(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
-                               const XfParams& xp, const CUtensorMap* tm, int B, cudaStream_t s);
+                               const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
 cudaError_t launch_input_run(int N, int alpha, int m, const float* x, float* V, const KGeom& g, const XfParams& xp,
-                             int B, cudaStream_t s);
+                             int nslab, cudaStream_t s);
 
 }  // namespace wino

@@ -21,11 +21,11 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
   constexpr int A1 = ipow(A, N - 1);
   constexpr int M1 = ipow(M, N - 1);
   constexpr int MN = ipow(M, N);
-  const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
   const int k = blockIdx.y;
   if (t >= g.T) return;
   const int64_t pstride = (int64_t)g.K * g.T_s;
-  const float* src = Mx + (int64_t)k * g.T_s + t;
+  const float* src = Mx + (int64_t)k * g.T_s + (t - g.t0);
   float o[MN];
 #pragma unroll
   for (int j = 0; j < MN; ++j) o[j] = 0.f;
@@ -88,7 +88,7 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
 
 template <int N, int A, int M, class Tab>
 cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams& xp, cudaStream_t s) {
-  dim3 grid((unsigned)((g.T + 127) / 128), (unsigned)g.K);
+  dim3 grid((unsigned)((g.T - g.t_beg + 127) / 128), (unsigned)g.K);
   k_output_xform<N, A, M, Tab><<<grid, 128, 0, s>>>(Mx, y, g, xp);
   return cudaGetLastError();
 }

@@ -36,10 +36,10 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def run(cfg, gemm_mode=0, points=None, batch=None, plan_batch=None):
+def run(cfg, gemm_mode=0, points=None, batch=None, plan_batch=None, fuse=0):
     x, g = make_inputs(cfg, batch=batch)
     plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, plan_batch or x.shape[0], cfg.padding,
-                    points=points, gemm_mode=gemm_mode)
+                    points=points, gemm_mode=gemm_mode, fuse=fuse)
     plan.filter_transform(g.cuda())
     y = plan.forward(x.cuda())
     torch.cuda.synchronize()
@@ -216,3 +216,18 @@ def test_gemm_resident_matches_streaming(name, monkeypatch):
     _, _, y_str, plan = run(cfg)
     plan.close()
     assert torch.equal(y_res, y_str)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("chunk_mb", ["0.05", "1"])
+def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
+    # the L2-chunked pipeline (fuse=4) runs the same per-tile arithmetic over
+    # slab ranges with chunk-local V/M rows: identical bits for any chunking
+    cfg = SMALL[name]
+    x, g, y0, plan = run(cfg)
+    plan.close()
+    monkeypatch.setenv("WINO_CHUNK_MB", chunk_mb)
+    _, _, y1, plan = run(cfg, fuse=wino.WINO_FUSE_L2_CHUNK)
+    chunks = plan.info["chunk_slabs"]
+    plan.close()
+    assert torch.equal(y0, y1), "chunk_slabs=%d" % chunks
