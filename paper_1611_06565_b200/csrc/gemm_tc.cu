@@ -422,6 +422,315 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 }
 
+
+// ---- A operand in TMEM ("TS" mode): the MMA reads only U from shared memory.
+// A (V_hi / V_lo chunk, 128 rows x kc columns) lives in TMEM columns, one tile
+// row t per lane; K-major by construction (a_major bit 15 = 0).
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_tf32_ts() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t u) { return (u + 0x1000u) & 0xFFFFE000u; }
+
+constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+// TS-mode GEMM.  Same units, U handling (resident or ring) and epilogue as
+// k_gemm_tc, but:
+//   raw ring:   V chunk [kc c][128 t] fp32, TMA box {128, kc} without swizzle;
+//   converter:  thread = tile row t (warp q owns TMEM lanes 32q..32q+31):
+//               reads its kc raw values (conflict-free 4-byte LDS), splits
+//               hi/lo in registers and writes them with tcgen05.st into one of
+//               two TMEM A stages (columns a0 + s*2kc: hi, +kc: lo);
+//   MMA:        tcgen05.mma ... [d], [a_tmem], b_desc (A from TMEM).
+// TMEM columns: 2*BN accumulators + 4*kc A stages.
+template <int BN, bool kRes>
+__global__ void __launch_bounds__(kThreads, 1)
+k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
+          const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
+          int C, int K, int kc, int three, int nraw, int nbr) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  const uint32_t sbase = sraw + pad;
+  const int n_chunks = (C + kc - 1) / kc;
+  const uint32_t a_bytes = (uint32_t)BM * kc * 4;
+  const uint32_t b_bytes = (uint32_t)BN * kc * 4;
+  const uint32_t raw0 = sbase;
+  const uint32_t bres = raw0 + nraw * a_bytes;
+  const uint32_t bres_bytes = kRes ? 2u * n_chunks * b_bytes : 2u * nbr * b_bytes;
+  const uint32_t bar0 = bres + bres_bytes;
+  auto rfull = [&](int s) { return bar0 + 8u * s; };
+  auto rempty = [&](int s) { return bar0 + 8u * (nraw + s); };
+  auto ufull = [&](int s) { return bar0 + 8u * (2 * nraw + s); };
+  auto uempty = [&](int s) { return bar0 + 8u * (2 * nraw + nbr + s); };
+  const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nbr);
+  auto tfull = [&](int a) { return bar1 + 8u * a; };
+  auto tempty = [&](int a) { return bar1 + 8u * (2 + a); };
+  auto afull = [&](int a) { return bar1 + 8u * (4 + a); };
+  auto aempty = [&](int a) { return bar1 + 8u * (6 + a); };
+  const uint32_t bfull = bar1 + 64u;
+  const uint32_t bempty = bar1 + 72u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar1 - sbase) + 80);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t kCols = pow2_cols(2 * BN + 4 * kc);
+  const uint32_t a_col0 = 2 * BN;
+
+  if (warp == 9) {
+    if (lane == 0) {
+      for (int s = 0; s < nraw; ++s) {
+        mbar_init(rfull(s), 1);
+        mbar_init(rempty(s), 128);
+      }
+      for (int s = 0; s < nbr; ++s) {
+        mbar_init(ufull(s), 1);
+        mbar_init(uempty(s), 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(tfull(a), 1);
+        mbar_init(tempty(a), 128);
+        mbar_init(afull(a), 128);
+        mbar_init(aempty(a), 1);
+      }
+      mbar_init(bfull, 1);
+      mbar_init(bempty, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int n_mblk = (T - t_lo + BM - 1) / BM;
+  const int n_nblk = (K + BN - 1) / BN;
+  const long long per_xi = (long long)n_nblk * n_mblk;
+  const long long total = (long long)P * per_xi;
+  long long u_beg, u_end, u_step;
+  if constexpr (kRes) {
+    u_beg = total * blockIdx.x / gridDim.x;
+    u_end = total * (blockIdx.x + 1) / gridDim.x;
+    u_step = 1;
+  } else {
+    u_beg = blockIdx.x;
+    u_end = total;
+    u_step = gridDim.x;
+  }
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- V producer (raw ring, one box per chunk)
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long u = u_beg; u < u_end; u += u_step) {
+        const int xi = (int)(u / per_xi);
+        const int mb = (int)(u % per_xi) % n_mblk;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          mbar_wait(rempty(s), ph ^ 1u);
+          mbar_expect_tx(rfull(s), a_bytes);
+          tma_load_3d(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s));
+          if (++s == nraw) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ---------------- U producer
+      if constexpr (kRes) {
+        long long cur_pair = -1;
+        int nload = 0;
+        for (long long u = u_beg; u < u_end; ++u) {
+          const long long pair = u / n_mblk;
+          if (pair == cur_pair) continue;
+          const int xi = (int)(u / per_xi);
+          const int nb = (int)(u % per_xi) / n_mblk;
+          if (nload > 0) mbar_wait(bempty, (uint32_t)((nload - 1) & 1));
+          mbar_expect_tx(bfull, (three ? 2u : 1u) * n_chunks * b_bytes);
+          for (int ch = 0; ch < n_chunks; ++ch)
+#pragma unroll
+            for (int gq = 0; gq < BN / 32; ++gq) {
+              tma_load_3d(bres + ch * b_bytes + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, bfull);
+              if (three)
+                tma_load_3d(bres + (n_chunks + ch) * b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi,
+                            bfull);
+            }
+          cur_pair = pair;
+          ++nload;
+        }
+      } else {
+        int s = 0;
+        uint32_t ph = 0;
+        for (long long u = u_beg; u < u_end; u += u_step) {
+          const int xi = (int)(u / per_xi);
+          const int nb = (int)(u % per_xi) / n_mblk;
+          for (int ch = 0; ch < n_chunks; ++ch) {
+            mbar_wait(uempty(s), ph ^ 1u);
+            const uint32_t st = bres + s * 2 * b_bytes;
+            mbar_expect_tx(ufull(s), (three ? 2u : 1u) * b_bytes);
+#pragma unroll
+            for (int gq = 0; gq < BN / 32; ++gq) {
+              tma_load_3d(st + gq * kc * 128, &tmBhi, nb * BN + gq * 32, ch * kc, xi, ufull(s));
+              if (three) tma_load_3d(st + b_bytes + gq * kc * 128, &tmBlo, nb * BN + gq * 32, ch * kc, xi, ufull(s));
+            }
+            if (++s == nbr) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32_ts<BN>();
+      const uint32_t lbo = (uint32_t)kc * 128u;
+      int as = 0, us = 0;
+      uint32_t aph = 0, uph = 0, acc = 0, cph = 0;
+      long long cur_pair = -1;
+      int nload = 0;
+      for (long long u = u_beg; u < u_end; u += u_step) {
+        if constexpr (kRes) {
+          const long long pair = u / n_mblk;
+          if (pair != cur_pair) {
+            mbar_wait(bfull, (uint32_t)(nload & 1));
+            tc_fence_after();
+            cur_pair = pair;
+            ++nload;
+          }
+        }
+        mbar_wait(tempty(acc), cph ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          mbar_wait(afull(as), aph);
+          if constexpr (!kRes) mbar_wait(ufull(us), uph);
+          tc_fence_after();
+          const uint32_t b_hi = kRes ? bres + ch * b_bytes : bres + us * 2 * b_bytes;
+          const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
+          uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
+          const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
+          for (int j = 0; j < kc / 8; ++j) {
+            const uint32_t accum = (ch | j) != 0;
+            if (three) {
+              tc_mma_tf32_ts(d, a_lo + 8 * j, dbh, idesc, accum);
+              tc_mma_tf32_ts(d, a_hi + 8 * j, dbl, idesc, 1u);
+              tc_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, 1u);
+            } else {
+              tc_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, accum);
+            }
+            dbh += 64; dbl += 64;
+          }
+          tc_commit(aempty(as));
+          as ^= 1;
+          if (as == 0) aph ^= 1u;
+          if constexpr (!kRes) {
+            tc_commit(uempty(us));
+            if (++us == nbr) { us = 0; uph ^= 1u; }
+          }
+        }
+        tc_commit(tfull(acc));
+        acc ^= 1u;
+        if (acc == 0) cph ^= 1u;
+        if constexpr (kRes) {
+          if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
+        }
+      }
+    }
+  } else if (warp < 4) {  // ---------------- converter: raw V row -> TMEM hi / lo
+    const int row = warp * 32 + lane;
+    const uint32_t lane_sel = (uint32_t)(warp * 32) << 16;
+    int rs = 0, as = 0;
+    uint32_t rph = 0, aph = 0;
+    for (long long u = u_beg; u < u_end; u += u_step) {
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        mbar_wait(rfull(rs), rph);
+        mbar_wait(aempty(as), aph ^ 1u);
+        tc_fence_after();
+        const float* raw = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
+        const uint32_t ahi = tmem_base + lane_sel + a_col0 + as * 2 * kc;
+        for (int cg = 0; cg < kc / 8; ++cg) {
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float v = raw[(cg * 8 + j) * BM];
+            const uint32_t h = tf32_rna_bits(__float_as_uint(v));
+            hi[j] = h;
+            lo[j] = tf32_rna_bits(__float_as_uint(v - __uint_as_float(h)));
+          }
+          tmem_st8(ahi + cg * 8, hi);
+          if (three) tmem_st8(ahi + kc + cg * 8, lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(rempty(rs));
+        mbar_arrive(afull(as));
+        if (++rs == nraw) { rs = 0; rph ^= 1u; }
+        as ^= 1;
+        if (as == 0) aph ^= 1u;
+      }
+    }
+  } else if (warp < 8) {  // warps 4-7 ------------------ epilogue
+    const int q = warp - 4;
+    uint32_t acc = 0, aph = 0;
+    for (long long u = u_beg; u < u_end; u += u_step) {
+      const int xi = (int)(u / per_xi);
+      const int rr = (int)(u % per_xi);
+      const int nb = rr / n_mblk, mb = rr % n_mblk;
+      mbar_wait(tfull(acc), aph);
+      tc_fence_after();
+      const int t = t_lo + mb * BM + q * 32 + lane;
+      float* out = Mo + ((long long)xi * K + (long long)nb * BN) * T_s + t;
+      const bool full_n = (nb + 1) * BN <= K;
+#pragma unroll 1
+      for (int cb = 0; cb < BN / 32; ++cb) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
+        if (t < T) {
+          float* p = out + (long long)cb * 32 * T_s;
+          if (full_n) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              __stcs(p, __uint_as_float(r[j]));
+              p += T_s;
+            }
+          } else {
+            const int kr = K - nb * BN - cb * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < kr) __stcs(p, __uint_as_float(r[j]));
+              p += T_s;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty(acc));
+      acc ^= 1u;
+      if (acc == 0) aph ^= 1u;
+    }
+  }
+  __syncthreads();
+  if (warp == 9) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kCols) : "memory");
+  }
+}
+
 }  // namespace tc
 
 // ---------------------------------------------------------------- host side
@@ -482,10 +791,58 @@ static TcSmem tc_smem(int bn, int kc, int C, bool res) {
   return t;
 }
 
+// TS-mode shared memory: raw V ring + U (resident or ring).
+static TcSmem ts_smem(int bn, int kc, int C, bool res) {
+  const int n_chunks = (C + kc - 1) / kc;
+  const size_t a = (size_t)tc::BM * kc * 4;
+  const size_t b2 = 2ull * bn * kc * 4;
+  const size_t fixed = 1024 + 1024;
+  const size_t budget = 232448;
+  TcSmem t{0, 0, 0, 0};
+  size_t left = budget - fixed;
+  if (res) {
+    const size_t bres = (size_t)n_chunks * b2;
+    if (bres + 2 * a > left) return t;
+    left -= bres;
+  } else {
+    int nbr = 4;
+    while (nbr > 1 && nbr * b2 + 3 * a > left) --nbr;
+    if (nbr * b2 + 2 * a > left) return t;
+    t.nbr = nbr;
+    left -= nbr * b2;
+  }
+  int nraw = (int)(left / a);
+  if (nraw > 8) nraw = 8;
+  t.nraw = nraw;
+  t.bytes = budget - (left - nraw * a);
+  return t;
+}
+
 template <int BN>
-static cudaError_t set_attr(size_t smem, bool res) {
-  return res ? cudaFuncSetAttribute(tc::k_gemm_tc<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-             : cudaFuncSetAttribute(tc::k_gemm_tc<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t set_attr(size_t smem, bool res, bool ts) {
+  const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (ts) return res ? cudaFuncSetAttribute(tc::k_gemm_ts<BN, true>, at, (int)smem)
+                     : cudaFuncSetAttribute(tc::k_gemm_ts<BN, false>, at, (int)smem);
+  return res ? cudaFuncSetAttribute(tc::k_gemm_tc<BN, true>, at, (int)smem)
+             : cudaFuncSetAttribute(tc::k_gemm_tc<BN, false>, at, (int)smem);
+}
+
+// V tensor map of the TS raw ring: box {128 t, kc c, 1}, no swizzle.
+static cudaError_t encode_v_ts(CUtensorMap* tm, const float* base, int64_t T_s, int C, int P, int kc) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {(cuuint64_t)T_s, (cuuint64_t)C, (cuuint64_t)P};
+  cuuint64_t strides[2] = {(cuuint64_t)T_s * 4, (cuuint64_t)T_s * 4 * C};
+  cuuint32_t box[3] = {(cuuint32_t)tc::BM, (cuuint32_t)kc, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+static TcSmem plan_smem(const TcGemm& tg, int C) {
+  return tg.ts ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
 }
 
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P, int64_t T_s,
@@ -497,21 +854,25 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   tg.num_sms = sms;
+  // TS mode (A in TMEM) when the accumulators and two A stages fit in TMEM
+  tg.ts = 2 * tg.bn + 4 * tg.kc <= 512;
+  if (const char* ev = getenv("WINO_GEMM_TS")) tg.ts = tg.ts && atoi(ev) != 0;
   // U-resident when the raw ring still gets >= 4 stages next to the U block
-  tg.resident = tc_smem(tg.bn, tg.kc, C, true).nraw >= 4;
+  tg.resident = (tg.ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
   if (const char* ev = getenv("WINO_GEMM_RES")) tg.resident = tg.resident && atoi(ev) != 0;
   cudaError_t e;
-  if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
+  if (tg.ts) e = encode_v_ts(&tg.tmA, V, T_s, C, P, tg.kc);
+  else e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc);
+  if (e != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
-  const TcSmem sm = tc_smem(tg.bn, tg.kc, C, tg.resident);
+  const TcSmem sm = plan_smem(tg, C);
   if (sm.nraw < 1) return cudaErrorInvalidConfiguration;
-  const size_t smem = sm.bytes;
   switch (tg.bn) {
-    case 32: e = set_attr<32>(smem, tg.resident); break;
-    case 64: e = set_attr<64>(smem, tg.resident); break;
-    case 128: e = set_attr<128>(smem, tg.resident); break;
-    default: e = set_attr<256>(smem, tg.resident); break;
+    case 32: e = set_attr<32>(sm.bytes, tg.resident, tg.ts); break;
+    case 64: e = set_attr<64>(sm.bytes, tg.resident, tg.ts); break;
+    case 128: e = set_attr<128>(sm.bytes, tg.resident, tg.ts); break;
+    default: e = set_attr<256>(sm.bytes, tg.resident, tg.ts); break;
   }
   if (e != cudaSuccess) return e;
   tg.ready = true;
@@ -521,18 +882,26 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
 template <int BN>
 static void launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P, int t_lo,
                       int T, int64_t T_s, int C, int K) {
-  if (tg.resident)
+  if (tg.ts) {
+    if (tg.resident)
+      tc::k_gemm_ts<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s,
+                                                                   C, K, tg.kc, tg.three, sm.nraw, sm.nbr);
+    else
+      tc::k_gemm_ts<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s,
+                                                                    C, K, tg.kc, tg.three, sm.nraw, sm.nbr);
+  } else if (tg.resident) {
     tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
                                                                  K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
-  else
+  } else {
     tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
                                                                   K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
+  }
 }
 
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s) {
   if (!tg.ready) return cudaErrorNotReady;
-  const TcSmem sm = tc_smem(tg.bn, tg.kc, C, tg.resident);
+  const TcSmem sm = plan_smem(tg, C);
   const long long units = (long long)P * ((K + tg.bn - 1) / tg.bn) * ((T - t_lo + tc::BM - 1) / tc::BM);
   const int grid = (int)(units < tg.num_sms ? units : tg.num_sms);
   if (grid <= 0) return cudaSuccess;

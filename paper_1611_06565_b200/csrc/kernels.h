@@ -37,6 +37,7 @@ struct TcGemm {
   int three;          // 1: 3xTF32, 0: 1xTF32
   int num_sms;
   bool resident;      // U block kept in shared memory (see k_gemm_tc)
+  bool ts;            // A operand (V_hi / V_lo) in TMEM (k_gemm_ts)
   bool ready;
 };
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,

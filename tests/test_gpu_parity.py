@@ -231,3 +231,16 @@ def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
     chunks = plan.info["chunk_slabs"]
     plan.close()
     assert torch.equal(y0, y1), "chunk_slabs=%d" % chunks
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+def test_gemm_tmem_a_matches_smem_a(name, monkeypatch):
+    # A operand (V_hi / V_lo) from TMEM (k_gemm_ts) vs from shared memory
+    # (k_gemm_tc): the same tf32 products in the same order -> identical bits
+    cfg = SMALL[name]
+    x, g, y_ts, plan = run(cfg)
+    plan.close()
+    monkeypatch.setenv("WINO_GEMM_TS", "0")
+    _, _, y_ss, plan = run(cfg)
+    plan.close()
+    assert torch.equal(y_ts, y_ss)
