@@ -96,4 +96,33 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
+// Programmatic dependent launch (PDL).  Kernels of the forward are launched
+// with programmatic stream serialization, so a kernel may start (prologue:
+// barrier init, TMEM alloc, descriptor prefetch) while its predecessor drains.
+// pdl_wait() blocks until every prerequisite grid has completed and its
+// memory is visible -- it must precede any access to data the predecessor
+// (or anything before it) produces or consumes; it is a no-op without PDL.
+// pdl_trigger() lets dependents launch once all CTAs of this grid issued it;
+// each kernel issues it only after its own pdl_wait (so dependents that run
+// early can rely on everything before this grid being complete).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch `kern` with the PDL attribute on stream s.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace wino

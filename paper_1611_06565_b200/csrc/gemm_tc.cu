@@ -204,6 +204,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();      // V comes from the input transform; M is read by the previous output transform
+  pdl_trigger();
 
   const int n_mblk = (T - t_lo + BM - 1) / BM;
   const int n_nblk = (K + BN - 1) / BN;
@@ -460,7 +462,7 @@ template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-          int C, int K, int kc, int three, int nraw, int nbr) {
+          int C, int K, int kc, int three, int nraw, int nbr, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
@@ -520,6 +522,8 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();      // V comes from the input transform; M is read by the previous output transform
+  pdl_trigger();
 
   const int n_mblk = (T - t_lo + BM - 1) / BM;
   const int n_nblk = (K + BN - 1) / BN;
@@ -623,7 +627,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
           uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
           const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
-          for (int j = 0; j < kc / 8; ++j) {
+          for (int j = 0; j < ((dbg & 4) ? 0 : kc / 8); ++j) {
             const uint32_t accum = (ch | j) != 0;
             if (three) {
               tc_mma_tf32_ts(d, a_lo + 8 * j, dbh, idesc, accum);
@@ -662,7 +666,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         const float* raw = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
         const uint32_t ahi = tmem_base + lane_sel + a_col0 + as * 2 * kc;
-        for (int cg = 0; cg < kc / 8; ++cg) {
+        for (int cg = 0; cg < ((dbg & 2) ? 0 : kc / 8); ++cg) {
           uint32_t hi[8], lo[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -699,7 +703,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int cb = 0; cb < BN / 32; ++cb) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
-        if (t < T) {
+        if (t < T && !(dbg & 1)) {
           float* p = out + (long long)cb * 32 * T_s;
           if (full_n) {
 #pragma unroll
@@ -857,9 +861,15 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   // TS mode (A in TMEM) when the accumulators and two A stages fit in TMEM
   tg.ts = 2 * tg.bn + 4 * tg.kc <= 512;
   if (const char* ev = getenv("WINO_GEMM_TS")) tg.ts = tg.ts && atoi(ev) != 0;
-  // U-resident when the raw ring still gets >= 4 stages next to the U block
-  tg.resident = (tg.ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
-  if (const char* ev = getenv("WINO_GEMM_RES")) tg.resident = tg.resident && atoi(ev) != 0;
+  tg.dbg = 0;  // dev-only experiment knob: 1 no M stores, 2 no V split, 4 no MMAs (results invalid)
+  if (const char* ev = getenv("WINO_GEMM_DBG")) tg.dbg = atoi(ev);
+  // U streamed through its ring by default: the grid-strided unit order keeps
+  // the 148 CTAs on neighbouring m-blocks (DRAM locality), measured faster
+  // than the U-resident contiguous ranges on every config; WINO_GEMM_RES=1
+  // selects U-resident where it fits
+  tg.resident = false;
+  if (const char* ev = getenv("WINO_GEMM_RES"))
+    tg.resident = atoi(ev) != 0 && (tg.ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
   cudaError_t e;
   if (tg.ts) e = encode_v_ts(&tg.tmA, V, T_s, C, P, tg.kc);
   else e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc);
@@ -880,22 +890,22 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
 }
 
 template <int BN>
-static void launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P, int t_lo,
-                      int T, int64_t T_s, int C, int K) {
+static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P,
+                             int t_lo, int T, int64_t T_s, int C, int K) {
+  const dim3 gd(grid), bd(tc::kThreads);
+  const long long Ts = T_s;
   if (tg.ts) {
     if (tg.resident)
-      tc::k_gemm_ts<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s,
-                                                                   C, K, tg.kc, tg.three, sm.nraw, sm.nbr);
-    else
-      tc::k_gemm_ts<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s,
-                                                                    C, K, tg.kc, tg.three, sm.nraw, sm.nbr);
-  } else if (tg.resident) {
-    tc::k_gemm_tc<BN, true><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
-                                                                 K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
-  } else {
-    tc::k_gemm_tc<BN, false><<<grid, tc::kThreads, sm.bytes, s>>>(tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, T_s, C,
-                                                                  K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
+      return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+                        C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
+    return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+                      C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
   }
+  if (tg.resident)
+    return launch_pdl(tc::k_gemm_tc<BN, true>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+                      C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
+  return launch_pdl(tc::k_gemm_tc<BN, false>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+                    C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
 }
 
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
@@ -906,12 +916,11 @@ cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int
   const int grid = (int)(units < tg.num_sms ? units : tg.num_sms);
   if (grid <= 0) return cudaSuccess;
   switch (tg.bn) {
-    case 32: launch_bn<32>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
-    case 64: launch_bn<64>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
-    case 128: launch_bn<128>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
-    default: launch_bn<256>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K); break;
+    case 32: return launch_bn<32>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
+    case 64: return launch_bn<64>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
+    case 128: return launch_bn<128>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
+    default: return launch_bn<256>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace wino

@@ -38,6 +38,7 @@ struct TcGemm {
   int num_sms;
   bool resident;      // U block kept in shared memory (see k_gemm_tc)
   bool ts;            // A operand (V_hi / V_lo) in TMEM (k_gemm_ts)
+  int dbg;            // dev-only experiment knob (WINO_GEMM_DBG), 0 in production
   bool ready;
 };
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,

@@ -154,6 +154,8 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   const int nt0 = min(g.bt0, g.tiles[0] - a0);
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
 
+  pdl_wait();      // x may come from the preceding kernel; V is read by the previous GEMM
+  pdl_trigger();
   // ---- 1. slab -> shared memory (zero fill outside the input)
   if constexpr (kTma) {
     static_assert(N >= 2, "TMA slab path needs N >= 2");
@@ -263,21 +265,18 @@ cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& 
     if (tm && g.dL == 0) {
       auto kern = k_input_xform<N, A, M, Tab, 0, true>;
       if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
-      kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, *tm);
-      return cudaGetLastError();
+      return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, *tm);
     }
     if (tm && g.dL == 3) {
       auto kern = k_input_xform<N, A, M, Tab, 3, true>;
       if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
-      kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, *tm);
-      return cudaGetLastError();
+      return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, *tm);
     }
   }
   auto kern = k_input_xform<N, A, M, Tab, 0, false>;
   if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
   CUtensorMap dummy{};
-  kern<<<grid, 256, g.slab_bytes, s>>>(x, V, g, xp, dummy);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, dummy);
 }
 
 template <int A, int M, class Tab, bool kAllowTma>

@@ -21,6 +21,8 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
   constexpr int A1 = ipow(A, N - 1);
   constexpr int M1 = ipow(M, N - 1);
   constexpr int MN = ipow(M, N);
+  pdl_wait();      // M comes from the GEMM
+  pdl_trigger();
   const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
   const int k = blockIdx.y;
   if (t >= g.T) return;
@@ -89,8 +91,7 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
 template <int N, int A, int M, class Tab>
 cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams& xp, cudaStream_t s) {
   dim3 grid((unsigned)((g.T - g.t_beg + 127) / 128), (unsigned)g.K);
-  k_output_xform<N, A, M, Tab><<<grid, 128, 0, s>>>(Mx, y, g, xp);
-  return cudaGetLastError();
+  return launch_pdl(k_output_xform<N, A, M, Tab>, grid, dim3(128), 0, s, Mx, y, g, xp);
 }
 
 template <int A, int M, class Tab>

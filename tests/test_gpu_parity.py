@@ -210,10 +210,10 @@ def test_gemm_resident_matches_streaming(name, monkeypatch):
     # the U-resident GEMM schedule and the streaming one issue the same MMAs
     # in the same order per output tile: identical bits
     cfg = SMALL[name]
-    x, g, y_res, plan = run(cfg)
+    x, g, y_str, plan = run(cfg)
     plan.close()
-    monkeypatch.setenv("WINO_GEMM_RES", "0")
-    _, _, y_str, plan = run(cfg)
+    monkeypatch.setenv("WINO_GEMM_RES", "1")
+    _, _, y_res, plan = run(cfg)
     plan.close()
     assert torch.equal(y_res, y_str)
 
