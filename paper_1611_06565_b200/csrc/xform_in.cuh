@@ -15,12 +15,13 @@
 //   1. stages the slab into shared memory: one TMA box load whose
 //      out-of-bounds fill supplies the zero padding (kTma), or coalesced
 //      4-byte cp.async (fallback for shapes that break a TMA rule),
-//   2. runs one work item per (xi_0, tile): the axis-0 combination
+//   2. N <= 2: one work item per tile, the whole window in registers; N >= 3:
+//      one work item per (xi_0, tile): the axis-0 combination
 //      h = sum_i B^T[xi_0][i] slab_row(i) (compile-time xi_0, so zero
 //      entries of B^T are skipped), then the remaining N-1 axes as register
-//      line transforms, reading window rows with 64/128-bit shared loads,
-//   3. writes the alpha^(N-1) values V[(xi_0, .)][c][t]; lanes hold
-//      consecutive t, so every warp store is one coalesced 128-byte line.
+//      line transforms; window rows are read with 64/128-bit shared loads,
+//   3. writes the values V[xi][c][t]; lanes hold consecutive t, so every warp
+//      store is one coalesced 128-byte line.
 //
 // TMA requires the innermost start coordinate to be 16-byte aligned
 // (measured: a start of -1 float faults, -4 works), so the TMA slab starts
@@ -76,6 +77,15 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     all_axes<A, 1, A, A, Get>(h, xp);
 #pragma unroll
     for (int j = 0; j < A; ++j) vout[j * pstride] = h[j];
+  } else if constexpr (N == 2) {
+    // the whole alpha x alpha window in registers: every window row is read
+    // once (no per-xi_0 re-reads), both axes transformed in place
+    float h[A * A];
+#pragma unroll
+    for (int i0 = 0; i0 < A; ++i0) load_row<A, M, D>(S + base + i0 * g.sst[0], h + i0 * A);
+    all_axes<A, 2, A, A, Get>(h, xp);
+#pragma unroll
+    for (int j = 0; j < A * A; ++j) vout[j * pstride] = h[j];
   } else {
     constexpr int NL = N - 1;            // axes handled in registers
     constexpr int P1 = ipow(A, NL);      // values per work item
@@ -226,7 +236,7 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
 
   // ---- 2./3. work items (xi_0, tile), tile fastest
   const int ntile = nt0 * g.R;
-  constexpr int NX = N >= 2 ? A : 1;
+  constexpr int NX = N >= 3 ? A : 1;  // work items per tile (one per xi_0 when N >= 3)
   const int64_t pstride = (int64_t)g.C * g.T_s;
   const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;  // V row of the slab's first tile
   float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
