@@ -27,6 +27,8 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
   const int k = blockIdx.y;
   if (t >= g.T) return;
   const int64_t pstride = (int64_t)g.K * g.T_s;
+  // running pointer over the alpha^N points (one 64-bit add per load instead
+  // of a 64-bit multiply-add per point offset)
   const float* src = Mx + (int64_t)k * g.T_s + (t - g.t0);
   float o[MN];
 #pragma unroll
@@ -35,7 +37,10 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
   for (int x1 = 0; x1 < A; ++x1) {
     float v[A1];
 #pragma unroll
-    for (int j = 0; j < A1; ++j) v[j] = __ldg(src + (x1 * A1 + j) * pstride);
+    for (int j = 0; j < A1; ++j) {
+      v[j] = __ldg(src);
+      src += pstride;
+    }
     all_axes<A, N - 1, M, M, ATget<Tab>>(v, xp);
 #pragma unroll
     for (int o1 = 0; o1 < M; ++o1) {
@@ -46,15 +51,16 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
         o[o1 * M1 + rr] = fmaf(av, v[digits_to_base(rr, N - 1, M, A)], o[o1 * M1 + rr]);
     }
   }
-  // scatter: tile t -> (b, t_1..t_N); outputs past `out` are discarded
-  int64_t rem = t;
+  // scatter: tile t -> (b, t_1..t_N) (32-bit: T < 2^31 is enforced at plan
+  // creation); outputs past `out` are discarded
+  int rem = (int)t;
   int gi[N];
 #pragma unroll
   for (int n = N - 1; n >= 0; --n) {
-    gi[n] = (int)(rem % g.tiles[n]);
+    gi[n] = rem % g.tiles[n];
     rem /= g.tiles[n];
   }
-  float* yb = y + (rem * g.K + k) * g.out_vol;
+  float* yb = y + ((int64_t)rem * g.K + k) * g.out_vol;
   const int lastpos = gi[N - 1] * M;
   const bool full_last = lastpos + M <= g.out[N - 1];
 #pragma unroll
@@ -65,7 +71,7 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
     for (int ax = 0; ax < N - 1; ++ax) {
       const int d = (rr / ipow(M, N - 2 - ax)) % M;
       const int pos = gi[ax] * M + d;
-      ok = ok && (pos < g.out[ax]);
+      ok = ok && (pos < (int)g.out[ax]);
       off += (int64_t)pos * g.out_stride[ax];
     }
     if (!ok) continue;
