@@ -120,10 +120,12 @@ WINO_API wino_status wino_filter_transform(wino_plan_t plan, const float* g, win
  * WINO_ERR_STATE if no filter transform (or mark_ready) happened. */
 WINO_API wino_status wino_forward(wino_plan_t plan, const float* x, float* y, int B, wino_stream_t stream);
 
-/* End-to-end variant with HOST buffers: copies x_host (B x C x in...) to a
- * plan-owned device buffer, runs wino_forward, copies y back to y_host and
- * synchronises `stream` before returning.  Host buffers should be pinned
- * (cudaHostAlloc / torch pin_memory) for full PCIe bandwidth. */
+/* End-to-end variant with HOST buffers x_host (B x C x in...) and y_host
+ * (B x K x out...).  The batch is split into up to 8 sample chunks pipelined
+ * over three streams (H2D copies, the forward on `stream`, D2H copies) into
+ * plan-owned device buffers, so both copy directions overlap the compute;
+ * synchronises before returning.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for full PCIe bandwidth and overlap. */
 WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, float* y_host, int B,
                               wino_stream_t stream);
 

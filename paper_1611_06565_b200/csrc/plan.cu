@@ -164,6 +164,7 @@ struct DeviceGuard {
 };
 
 constexpr int kMaxProf = 4096;
+constexpr int kHostChunks = 16;  // wino_forward_host pipeline depth
 
 }  // namespace
 
@@ -181,7 +182,9 @@ struct wino_plan_s {
   size_t filter_bytes = 0, filter_bcast_bytes = 0;
   float *V = nullptr, *M = nullptr;
   size_t ws_bytes = 0;
-  float *x_dev = nullptr, *y_dev = nullptr;
+  float *x_dev = nullptr, *y_dev = nullptr;   // wino_forward_host staging
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t e_in[kHostChunks]{}, e_fw[kHostChunks]{}, e_start = nullptr;
   bool filter_ready = false;
   TcGemm tg{};
   CUtensorMap tm_x{};          // input-transform TMA map (cached per x pointer / B)
@@ -376,6 +379,15 @@ wino_status wino_plan_destroy(wino_plan_t p) {
   cudaFree(p->x_dev);
   cudaFree(p->y_dev);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+  if (p->s_in) {
+    for (int i = 0; i < kHostChunks; ++i) {
+      cudaEventDestroy(p->e_in[i]);
+      cudaEventDestroy(p->e_fw[i]);
+    }
+    cudaEventDestroy(p->e_start);
+    cudaStreamDestroy(p->s_in);
+    cudaStreamDestroy(p->s_out);
+  }
   delete p;
   return WINO_OK;
 }
@@ -467,22 +479,54 @@ wino_status wino_forward(wino_plan_t p, const float* x, float* y, int B, wino_st
   return forward_impl(p, x, y, B, (cudaStream_t)stream);
 }
 
+// Host-buffer forward: the batch is split into sample chunks and pipelined
+// over three streams -- H2D copies (s_in), the forward kernels (the caller's
+// stream), D2H copies (s_out) -- so PCIe traffic in both directions overlaps
+// the compute and each other.  Chunks share the plan workspace, so their
+// forwards stay ordered on the compute stream.  Synchronises before return.
 wino_status wino_forward_host(wino_plan_t p, const float* x_host, float* y_host, int B, wino_stream_t stream) {
   if (!p || !x_host || !y_host) return fail(WINO_ERR_ARG, "NULL plan, x_host or y_host");
   if (B < 1 || B > p->batch) return fail(WINO_ERR_ARG, "B=%d outside 1..%d (planned batch)", B, p->batch);
   if (!p->filter_ready) return fail(WINO_ERR_STATE, "forward before wino_filter_transform / mark_ready");
   DeviceGuard guard(p->device);
-  const size_t xb = (size_t)p->batch * p->C * p->geom.in_vol * 4;
-  const size_t yb = (size_t)p->batch * p->K * p->geom.out_vol * 4;
-  if (!p->x_dev) CUDA_TRY(cudaMalloc(&p->x_dev, xb));
-  if (!p->y_dev) CUDA_TRY(cudaMalloc(&p->y_dev, yb));
+  const size_t xs = (size_t)p->C * p->geom.in_vol;   // floats per sample
+  const size_t ys = (size_t)p->K * p->geom.out_vol;
+  if (!p->x_dev) CUDA_TRY(cudaMalloc(&p->x_dev, (size_t)p->batch * xs * 4));
+  if (!p->y_dev) CUDA_TRY(cudaMalloc(&p->y_dev, (size_t)p->batch * ys * 4));
+  if (!p->s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < kHostChunks; ++i) {
+      CUDA_TRY(cudaEventCreateWithFlags(&p->e_in[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&p->e_fw[i], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&p->e_start, cudaEventDisableTiming));
+  }
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t xn = (size_t)B * p->C * p->geom.in_vol * 4;
-  const size_t yn = (size_t)B * p->K * p->geom.out_vol * 4;
-  CUDA_TRY(cudaMemcpyAsync(p->x_dev, x_host, xn, cudaMemcpyHostToDevice, s));
-  wino_status st = forward_impl(p, p->x_dev, p->y_dev, B, s);
-  if (st) return st;
-  CUDA_TRY(cudaMemcpyAsync(y_host, p->y_dev, yn, cudaMemcpyDeviceToHost, s));
+  // 8 chunks (measured best or within 3% of best on c2-c5, tools/e2e_probe.py);
+  // WINO_HOST_CHUNKS overrides
+  int nch = 8;
+  if (const char* ev = getenv("WINO_HOST_CHUNKS")) nch = atoi(ev);
+  if (nch < 1) nch = 1;
+  if (nch > kHostChunks) nch = kHostChunks;
+  if (nch > B) nch = B;
+  // the copy streams start after everything already queued on the caller's stream
+  CUDA_TRY(cudaEventRecord(p->e_start, s));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->e_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->e_start, 0));
+  for (int i = 0; i < nch; ++i) {
+    const int b0 = (int)((int64_t)B * i / nch), b1 = (int)((int64_t)B * (i + 1) / nch);
+    const size_t nb = (size_t)(b1 - b0);
+    CUDA_TRY(cudaMemcpyAsync(p->x_dev + b0 * xs, x_host + b0 * xs, nb * xs * 4, cudaMemcpyHostToDevice, p->s_in));
+    CUDA_TRY(cudaEventRecord(p->e_in[i], p->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(s, p->e_in[i], 0));
+    wino_status st = forward_impl(p, p->x_dev + b0 * xs, p->y_dev + b0 * ys, (int)nb, s);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(p->e_fw[i], s));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->e_fw[i], 0));
+    CUDA_TRY(cudaMemcpyAsync(y_host + b0 * ys, p->y_dev + b0 * ys, nb * ys * 4, cudaMemcpyDeviceToHost, p->s_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->s_out));
   CUDA_TRY(cudaStreamSynchronize(s));
   return WINO_OK;
 }
