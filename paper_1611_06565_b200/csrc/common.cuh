@@ -51,7 +51,11 @@ struct KGeom {
   int dL;                    // TMA column shift of the slab rows (0 or 3)
   int sst[kMaxN];            // slab element strides (sst[N-1] = 1)
   int R;                     // tiles per axis-0 slice: prod_{n>=1} tiles[n]
-  int slab_bytes;            // dynamic shared memory of the input kernel
+  int slab_bytes;            // bytes of the slab (one TMA box)
+  int slot_bytes;            // slab slot stride (slab_bytes rounded up to 128)
+  int hpitch;                // N = 3, alpha >= 6: row pitch of the axis-0 pass buffer H
+  int nslot;                 // slab slots: 2 = persistent CTAs prefetching the next plane
+  int smem_bytes;            // dynamic shared memory of the input kernel (nslot slabs + H)
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

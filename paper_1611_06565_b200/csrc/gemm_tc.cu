@@ -25,103 +25,11 @@
 #include <cstdlib>
 
 #include "kernels.h"
+#include "tc_common.cuh"
 #include "tma.hpp"
 
 namespace wino {
 namespace tc {
-
-constexpr int BM = 128;
-constexpr int kThreads = 352;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
-// Shared-memory matrix descriptor for the canonical MN-major tf32 layout
-// SWIZZLE_128B_BASE32B (layout type 1; fp32 MN-major operands require the
-// 32-byte swizzle base): rows of 128 B = 32 MN elements, 32-byte chunks XORed
-// with (row mod 4), 4 K-rows (512 B) per swizzle atom.
-//   LBO = byte distance between 32-element groups along MN,
-//   SBO = byte distance between 4-row atoms along K (512 when dense).
-// Bits: addr>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
-// layout type [61,64).  The TMA side writes the same pattern with
-// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
-  return d;
-}
-
-// Instruction descriptor kind::tf32: D f32 (bit 4), A/B tf32 (=2 at bits 7, 10),
-// A and B MN-major (bits 15, 16), N>>3 at bit 17, M>>4 at bit 24.
-template <int BN>
-__host__ __device__ constexpr uint32_t idesc_tf32() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-constexpr uint32_t tmem_cols(int bn) {
-  return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
-}
 
 // Work unit u = (xi, n-block, m-block), m-block fastest.  Two shared-memory
 // rings decouple HBM latency from the tensor core:
@@ -425,30 +333,6 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 }
 
 
-// ---- A operand in TMEM ("TS" mode): the MMA reads only U from shared memory.
-// A (V_hi / V_lo chunk, 128 rows x kc columns) lives in TMEM columns, one tile
-// row t per lane; K-major by construction (a_major bit 15 = 0).
-template <int BN>
-__host__ __device__ constexpr uint32_t idesc_tf32_ts() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-}
-__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                               uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
-__device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t u) { return (u + 0x1000u) & 0xFFFFE000u; }
-
-constexpr uint32_t pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
-
 // TS-mode GEMM.  Same units, U handling (resident or ring) and epilogue as
 // k_gemm_tc, but:
 //   raw ring:   V chunk [kc c][128 t] fp32, TMA box {128, kc} without swizzle;
@@ -482,14 +366,17 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nbr);
   auto tfull = [&](int a) { return bar1 + 8u * a; };
   auto tempty = [&](int a) { return bar1 + 8u * (2 + a); };
-  auto afull = [&](int a) { return bar1 + 8u * (4 + a); };
-  auto aempty = [&](int a) { return bar1 + 8u * (6 + a); };
-  const uint32_t bfull = bar1 + 64u;
-  const uint32_t bempty = bar1 + 72u;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar1 - sbase) + 80);
+  auto afull = [&](int a) { return bar1 + 8u * (4 + a); };   // a < 4
+  auto aempty = [&](int a) { return bar1 + 8u * (8 + a); };
+  const uint32_t bfull = bar1 + 96u;   // after afull(0..3) at +32, aempty(0..3) at +64
+  const uint32_t bempty = bar1 + 104u;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar1 - sbase) + 112);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t kCols = pow2_cols(2 * BN + 4 * kc);
+  // TMEM: 2 accumulators + na A stages (V_hi | V_lo), na in [2, 4]
+  int na = (512 - 2 * BN) / (2 * kc);
+  na = na > 4 ? 4 : na;
+  const uint32_t kCols = pow2_cols(2 * BN + 2 * kc * na);
   const uint32_t a_col0 = 2 * BN;
 
   if (warp == 9) {
@@ -505,6 +392,8 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int a = 0; a < 2; ++a) {
         mbar_init(tfull(a), 1);
         mbar_init(tempty(a), 128);
+      }
+      for (int a = 0; a < na; ++a) {
         mbar_init(afull(a), 128);
         mbar_init(aempty(a), 1);
       }
@@ -639,8 +528,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             dbh += 64; dbl += 64;
           }
           tc_commit(aempty(as));
-          as ^= 1;
-          if (as == 0) aph ^= 1u;
+          if (++as == na) { as = 0; aph ^= 1u; }
           if constexpr (!kRes) {
             tc_commit(uempty(us));
             if (++us == nbr) { us = 0; uph ^= 1u; }
@@ -683,8 +571,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_arrive(rempty(rs));
         mbar_arrive(afull(as));
         if (++rs == nraw) { rs = 0; rph ^= 1u; }
-        as ^= 1;
-        if (as == 0) aph ^= 1u;
+        if (++as == na) { as = 0; aph ^= 1u; }
       }
     }
   } else if (warp < 8) {  // warps 4-7 ------------------ epilogue
@@ -790,6 +677,7 @@ static TcSmem tc_smem(int bn, int kc, int C, bool res) {
   }
   int nraw = (int)(left / a);
   if (nraw > 8) nraw = 8;
+  if (const char* ev = getenv("WINO_GEMM_NRAW")) nraw = nraw < atoi(ev) ? nraw : atoi(ev);  // dev knob
   t.nraw = nraw;
   t.bytes = budget - (left - nraw * a);
   return t;
@@ -810,6 +698,7 @@ static TcSmem ts_smem(int bn, int kc, int C, bool res) {
     left -= bres;
   } else {
     int nbr = 4;
+    if (const char* ev = getenv("WINO_GEMM_NBR")) nbr = atoi(ev);  // dev knob
     while (nbr > 1 && nbr * b2 + 3 * a > left) --nbr;
     if (nbr * b2 + 2 * a > left) return t;
     t.nbr = nbr;
@@ -817,6 +706,7 @@ static TcSmem ts_smem(int bn, int kc, int C, bool res) {
   }
   int nraw = (int)(left / a);
   if (nraw > 8) nraw = 8;
+  if (const char* ev = getenv("WINO_GEMM_NRAW")) nraw = nraw < atoi(ev) ? nraw : atoi(ev);  // dev knob
   t.nraw = nraw;
   t.bytes = budget - (left - nraw * a);
   return t;
@@ -846,7 +736,7 @@ static cudaError_t encode_v_ts(CUtensorMap* tm, const float* base, int64_t T_s, 
 }
 
 static TcSmem plan_smem(const TcGemm& tg, int C) {
-  return tg.ts ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
+  return tg.variant == kGemmTS ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
 }
 
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P, int64_t T_s,
@@ -854,37 +744,45 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   tg.ready = false;
   tg.bn = pick_bn(K);
   tg.kc = C >= 32 ? 32 : ((C + 7) / 8) * 8;
+  if (const char* ev = getenv("WINO_GEMM_KC")) tg.kc = atoi(ev);  // dev knob (8, 16, 32)
   tg.three = three;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   tg.num_sms = sms;
-  // TS mode (A in TMEM) when the accumulators and two A stages fit in TMEM
-  tg.ts = 2 * tg.bn + 4 * tg.kc <= 512;
-  if (const char* ev = getenv("WINO_GEMM_TS")) tg.ts = tg.ts && atoi(ev) != 0;
-  tg.dbg = 0;  // dev-only experiment knob: 1 no M stores, 2 no V split, 4 no MMAs (results invalid)
-  if (const char* ev = getenv("WINO_GEMM_DBG")) tg.dbg = atoi(ev);
+  // TS mode (A in TMEM) when the accumulators and two A stages fit in TMEM;
+  // CTA pairs (cta_group::2) on top of TS
+  tg.can_ts = 2 * tg.bn + 4 * tg.kc <= 512;
+  tg.can_pair = tg.can_ts && ts2_supported(tg.bn, tg.kc);
+  tg.variant = tg.can_ts ? kGemmTS : kGemmSS;
   // U streamed through its ring by default: the grid-strided unit order keeps
-  // the 148 CTAs on neighbouring m-blocks (DRAM locality), measured faster
-  // than the U-resident contiguous ranges on every config; WINO_GEMM_RES=1
-  // selects U-resident where it fits
+  // the CTAs on neighbouring m-blocks (DRAM locality), measured faster than
+  // the U-resident contiguous ranges; WINO_GEMM_RES=1 selects U-resident
   tg.resident = false;
   if (const char* ev = getenv("WINO_GEMM_RES"))
-    tg.resident = atoi(ev) != 0 && (tg.ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
+    tg.resident = atoi(ev) != 0 && (tg.can_ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
+  tg.dbg = 0;  // dev-only experiment knob: 1 no M stores, 2 no V split, 4 no MMAs (results invalid)
+  if (const char* ev = getenv("WINO_GEMM_DBG")) tg.dbg = atoi(ev);
   cudaError_t e;
-  if (tg.ts) e = encode_v_ts(&tg.tmA, V, T_s, C, P, tg.kc);
-  else e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc);
-  if (e != cudaSuccess) return e;
+  if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
+  if (tg.can_ts && (e = encode_v_ts(&tg.tmA_ts, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
   if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
-  const TcSmem sm = plan_smem(tg, C);
-  if (sm.nraw < 1) return cudaErrorInvalidConfiguration;
-  switch (tg.bn) {
-    case 32: e = set_attr<32>(sm.bytes, tg.resident, tg.ts); break;
-    case 64: e = set_attr<64>(sm.bytes, tg.resident, tg.ts); break;
-    case 128: e = set_attr<128>(sm.bytes, tg.resident, tg.ts); break;
-    default: e = set_attr<256>(sm.bytes, tg.resident, tg.ts); break;
+  for (int ts = 0; ts <= (tg.can_ts ? 1 : 0); ++ts) {
+    const TcSmem sm = ts ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
+    if (sm.nraw < 1) {
+      if (!ts) return cudaErrorInvalidConfiguration;
+      tg.can_ts = tg.can_pair = false;
+      tg.variant = kGemmSS;
+      break;
+    }
+    switch (tg.bn) {
+      case 32: e = set_attr<32>(sm.bytes, tg.resident, ts); break;
+      case 64: e = set_attr<64>(sm.bytes, tg.resident, ts); break;
+      case 128: e = set_attr<128>(sm.bytes, tg.resident, ts); break;
+      default: e = set_attr<256>(sm.bytes, tg.resident, ts); break;
+    }
+    if (e != cudaSuccess) return e;
   }
-  if (e != cudaSuccess) return e;
   tg.ready = true;
   return cudaSuccess;
 }
@@ -894,11 +792,11 @@ static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaS
                              int t_lo, int T, int64_t T_s, int C, int K) {
   const dim3 gd(grid), bd(tc::kThreads);
   const long long Ts = T_s;
-  if (tg.ts) {
+  if (tg.variant == kGemmTS) {
     if (tg.resident)
-      return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+      return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bd, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
                         C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
-    return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+    return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bd, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
                       C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
   }
   if (tg.resident)
@@ -911,6 +809,7 @@ static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaS
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s) {
   if (!tg.ready) return cudaErrorNotReady;
+  if (tg.variant == kGemmPair) return launch_gemm_ts2(tg, Mo, P, t_lo, T, T_s, C, K, s);
   const TcSmem sm = plan_smem(tg, C);
   const long long units = (long long)P * ((K + tg.bn - 1) / tg.bn) * ((T - t_lo + tc::BM - 1) / tc::BM);
   const int grid = (int)(units < tg.num_sms ? units : tg.num_sms);
@@ -921,6 +820,43 @@ cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int
     case 128: return launch_bn<128>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
     default: return launch_bn<256>(tg, grid, sm, s, Mo, P, (int)t_lo, (int)T, T_s, C, K);
   }
+}
+
+cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K) {
+  if (const char* ev = getenv("WINO_GEMM_VARIANT")) {
+    const int v = atoi(ev);
+    if ((v == kGemmTS && tg.can_ts) || (v == kGemmPair && tg.can_pair) || v == kGemmSS) tg.variant = v;
+    return cudaSuccess;
+  }
+  if (const char* ev = getenv("WINO_GEMM_PAIR"))  // dev knob: pair on/off without timing
+    if (!atoi(ev)) { tg.variant = tg.can_ts ? kGemmTS : kGemmSS; return cudaSuccess; }
+  int cand[3], nc = 0;
+  cand[nc++] = kGemmSS;
+  if (tg.can_ts) cand[nc++] = kGemmTS;
+  if (tg.can_pair) cand[nc++] = kGemmPair;
+  if (nc == 1) { tg.variant = kGemmSS; return cudaSuccess; }
+  cudaEvent_t e0, e1;
+  cudaError_t e;
+  if ((e = cudaEventCreate(&e0)) != cudaSuccess) return e;
+  if ((e = cudaEventCreate(&e1)) != cudaSuccess) return e;
+  float best = 1e30f;
+  int best_v = cand[0];
+  for (int i = 0; i < nc; ++i) {
+    tg.variant = cand[i];
+    if ((e = launch_gemm_tc(tg, Mo, P, 0, T, T_s, C, K, 0)) != cudaSuccess) break;  // warm-up
+    float t = 0.f;
+    cudaEventRecord(e0, 0);
+    for (int r = 0; r < 3; ++r) launch_gemm_tc(tg, Mo, P, 0, T, T_s, C, K, 0);
+    cudaEventRecord(e1, 0);
+    if ((e = cudaEventSynchronize(e1)) != cudaSuccess) break;
+    cudaEventElapsedTime(&t, e0, e1);
+    if (t < best) { best = t; best_v = cand[i]; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  tg.variant = best_v;
+  if (getenv("WINO_DEBUG")) fprintf(stderr, "[wino] gemm variant %d (%.4f ms per launch)\n", best_v, best / 3);
+  return e;
 }
 
 }  // namespace wino

@@ -28,21 +28,33 @@ cudaError_t launch_gemm_ffma(const float* V, const float* U32, float* Mo, int P,
                              int C, int K, int K_s, cudaStream_t s);
 
 // a3 on tcgen05 tensor cores.
+// GEMM variants (all compute the same products in the same order per output
+// row -> bit-identical results; the plan times the supported ones once and
+// keeps the fastest, see tc_gemm_tune).
+enum { kGemmSS = 0, kGemmTS = 1, kGemmPair = 2 };
 struct TcGemm {
-  CUtensorMap tmA;    // V   [P][C][T_s]   (3-D map: t, c, xi)
+  CUtensorMap tmA;    // V   [P][C][T_s]   (t, c, xi): 32 x kc boxes, 128B swizzle (SS mode)
+  CUtensorMap tmA_ts; // V   128 x kc boxes, no swizzle (TS / pair modes: raw V ring)
   CUtensorMap tmBhi;  // U_hi [P][C][K_s]
   CUtensorMap tmBlo;  // U_lo
   int bn;             // N tile (32, 64, 128, 256)
   int kc;             // channels per pipeline stage (multiple of 8, <= 32)
   int three;          // 1: 3xTF32, 0: 1xTF32
   int num_sms;
-  bool resident;      // U block kept in shared memory (see k_gemm_tc)
-  bool ts;            // A operand (V_hi / V_lo) in TMEM (k_gemm_ts)
+  bool resident;      // U block kept in shared memory (SS / TS modes)
+  int variant;        // kGemmSS, kGemmTS or kGemmPair
+  bool can_ts, can_pair;
   int dbg;            // dev-only experiment knob (WINO_GEMM_DBG), 0 in production
   bool ready;
 };
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,
                             int64_t T_s, int C, int K_s, int K, int three, int device);
+// Time every supported variant on the plan's workspace (rows [0, T)) and keep
+// the fastest; WINO_GEMM_VARIANT=0/1/2 forces one.  Synchronises the device.
+cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K);
+bool ts2_supported(int bn, int kc);
+cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
+                            cudaStream_t s);
 // rows [t_lo, T) of every point (t_lo a multiple of 4)
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s);

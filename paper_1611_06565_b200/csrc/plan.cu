@@ -357,6 +357,7 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   if (tc) {
     e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
                         p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
+    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
@@ -546,8 +547,9 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
-  const int64_t v[16] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
-                         p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0};
+  const int64_t v[18] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+                         p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
+                         p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

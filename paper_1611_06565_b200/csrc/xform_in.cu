@@ -1,5 +1,7 @@
 // xform_in.cu -- host side of stage a2: slab geometry, the TMA descriptor of
 // x, and dispatch to the instantiations (xform_in_const.cu, xform_in_run.cu).
+#include <cstdlib>
+
 #include "tma.hpp"
 #include "xform_in.cuh"
 
@@ -30,20 +32,45 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
     }
   }
   g.sst[0] = inner;
-  const size_t kTarget = 64 * 1024, kMax = 200 * 1024;
-  auto bytes = [&](int bt) {
+  // N = 3, alpha >= 6: H = axis-0 pass of the slab, [bt0][alpha][e1][hpitch]
+  const bool hmode = N == 3 && alpha >= 6;
+  g.hpitch = hmode ? (g.e[2] + 3) / 4 * 4 : 0;
+  auto slab = [&](int bt) {
     const int e0 = bt * m + halo;
     if (N == 1) return (size_t)((e0 + 3) / 4 * 4) * 4;
     return (size_t)e0 * inner * 4;
   };
+  auto hbytes = [&](int bt) { return hmode ? (size_t)bt * alpha * g.e[1] * g.hpitch * 4 : (size_t)0; };
+  // TMA path: two slab slots (persistent CTAs prefetch the next plane) if
+  // 2 slabs + H fit ~76 KB (3 CTAs / SM) for some bt0; else one slot, slab
+  // (+ H) near 64 KB (100 KB with H).
   int bt0 = g.tiles[0];
-  while (bt0 > 1 && bytes(bt0) > kTarget) bt0 = (bt0 + 1) / 2;
-  if (bytes(bt0) > kMax) return false;
+  int nslot = 1;
+  // measured (c2, c4): the persistent prefetching variant is slower than
+  // one-shot CTAs; WINO_IN_SLOTS=2 enables it for experiments
+  const char* ev_slots = getenv("WINO_IN_SLOTS");
+  if (tma && N >= 2 && ev_slots && atoi(ev_slots) == 2) {
+    int bt = g.tiles[0];
+    while (bt > 1 && 2 * slab(bt) + hbytes(bt) > 76 * 1024) bt = (bt + 1) / 2;
+    if (2 * slab(bt) + hbytes(bt) <= 100 * 1024) {
+      nslot = 2;
+      bt0 = bt;
+    }
+  }
+  if (nslot == 1) {
+    size_t target = hmode ? 48 * 1024 : 64 * 1024;  // measured: c4 (H mode) 337 -> 288 us at bt0 = 1
+    if (const char* ev = getenv("WINO_IN_TARGET_KB")) target = (size_t)atoi(ev) * 1024;  // dev knob
+    while (bt0 > 1 && slab(bt0) + hbytes(bt0) > target) bt0 = (bt0 + 1) / 2;
+  }
+  if (nslot * (slab(bt0) + 128) + hbytes(bt0) > 200 * 1024) return false;
   g.bt0 = bt0;
+  g.nslot = nslot;
   g.nbox0 = (g.tiles[0] + bt0 - 1) / bt0;
   g.e[0] = bt0 * m + halo;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
-  g.slab_bytes = (int)bytes(bt0);
+  g.slab_bytes = (int)slab(bt0);
+  g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
+  g.smem_bytes = (int)(nslot * g.slot_bytes + hbytes(bt0));
   return true;
 }
 

@@ -150,48 +150,11 @@ __device__ __forceinline__ void tma_load_slab(uint32_t dst, const CUtensorMap* t
   }
 }
 
-// kTma (N >= 2): slab via one TMA box starting D columns left of -P_last.
-// !kTma: cp.async fallback, D == 0.
-template <int N, int A, int M, class Tab, int D, bool kTma>
-__global__ void __launch_bounds__(256)
-k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
-              const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm) {
-  extern __shared__ __align__(128) float S[];
-  __shared__ __align__(8) uint64_t bar;
-  const int64_t slab = g.s_beg + blockIdx.x;
-  const int b = (int)(slab / g.nbox0), box = (int)(slab - (int64_t)b * g.nbox0), c = blockIdx.y;
-  const int a0 = box * g.bt0;
-  const int nt0 = min(g.bt0, g.tiles[0] - a0);
+// Load plane (b, box, c)'s slab with cp.async (fallback path, D == 0).
+template <int N, int A, int M>
+__device__ __forceinline__ void load_slab_cpasync(float* S, const float* __restrict__ x, const KGeom& g, int b,
+                                                  int a0, int nt0, int c) {
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
-
-  pdl_wait();      // x may come from the preceding kernel; V is read by the previous GEMM
-  pdl_trigger();
-  // ---- 1. slab -> shared memory (zero fill outside the input)
-  if constexpr (kTma) {
-    static_assert(N >= 2, "TMA slab path needs N >= 2");
-    const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&bar);
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      int co[5];
-      co[0] = -g.pad[N - 1] - D;
-#pragma unroll
-      for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : 0) - g.pad[ax];
-      co[N] = b * g.C + c;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(g.slab_bytes) : "memory");
-      tma_load_slab(sbase, &tm, co, mb, N + 1);
-    }
-    __syncthreads();
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(mb)
-          : "memory");
-    }
-  } else {
-    static_assert(D == 0, "the cp.async slab path is unshifted");
     const int e0 = nt0 * M + (A - M);
     const float* __restrict__ xb = x + ((int64_t)b * g.C + c) * g.in_vol;
     int rows = N == 1 ? 1 : e0;
@@ -230,29 +193,184 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
         else drow[col] = 0.f;
       }
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Issue the TMA box of plane (b, box, c) into slab S (thread 0 only).
+template <int N, int M, int D>
+__device__ __forceinline__ void issue_slab_tma(float* S, const CUtensorMap* tm, const KGeom& g, int b, int a0, int c,
+                                               uint32_t bar) {
+  int co[5];
+  co[0] = -g.pad[N - 1] - D;
+#pragma unroll
+  for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : 0) - g.pad[ax];
+  co[N] = b * g.C + c;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(g.slab_bytes) : "memory");
+  tma_load_slab((uint32_t)__cvta_generic_to_shared(S), tm, co, bar, N + 1);
+}
+
+// Transform one staged plane: slab S -> V rows of tiles [a0, a0 + nt0) x (all).
+template <int N, int A, int M, class Tab, int D>
+__device__ __forceinline__ void transform_plane(const float* __restrict__ S, float* __restrict__ H, float* __restrict__ V,
+                                                const KGeom& g, const XfParams& xp, int b, int a0, int nt0, int c) {
+  // ---- N = 3, alpha >= 6: the axis-0 pass materialised in shared memory
+  if constexpr (N == 3 && A >= 6) {
+    using Get = BTget<Tab>;
+    const int e1 = g.e[1], e2 = g.e[2], hp = g.hpitch;
+    // H: [t0][xi_0][y][x], window rows 16-byte aligned
+    // phase 1: one thread per (t0, y, x) column: alpha values along axis 0
+    // (conflict-free scalar LDS, lanes = consecutive x) -> alpha xi_0 outputs
+    for (int w = threadIdx.x; w < nt0 * e1 * hp; w += blockDim.x) {
+      const int xh = w % hp, r = w / hp;
+      if (xh >= e2) continue;
+      const int y = r % e1, t0l = r / e1;
+      const float* col = S + t0l * M * g.sst[0] + y * g.sst[1] + xh + D;
+      float v[A];
+#pragma unroll
+      for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
+      float* hrow = H + (t0l * A * e1 + y) * hp + xh;
+#pragma unroll
+      for (int x0 = 0; x0 < A; ++x0) {
+        float acc = 0.f;
+        bool first = true;
+#pragma unroll
+        for (int i = 0; i < A; ++i) {
+          if (Get::nz(xp, x0, i)) {
+            acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
+            first = false;
+          }
+        }
+        hrow[x0 * e1 * hp] = acc;
+      }
+    }
     __syncthreads();
-  }
+    // phase 2: one work item per (t0, xi_0, t1, t2): the alpha x alpha window
+    // of plane (t0, xi_0) in registers, axes 1 and 2 transformed in place
+    const int tl1 = g.tiles[1], tl2 = g.tiles[2];
+    const int64_t pstride = (int64_t)g.C * g.T_s;
+    const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;
+    float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
+    for (int w = threadIdx.x; w < nt0 * A * tl1 * tl2; w += blockDim.x) {
+      const int t2 = w % tl2;
+      int r = w / tl2;
+      const int t1 = r % tl1;
+      r /= tl1;
+      const int xi0 = r % A, t0l = r / A;
+      const float* hp0 = H + ((t0l * A + xi0) * e1 + t1 * M) * hp + t2 * M;
+      float h[A * A];
+#pragma unroll
+      for (int i1 = 0; i1 < A; ++i1) load_row<A, M, 0>(hp0 + i1 * hp, h + i1 * A);
+      all_axes<A, 2, A, A, Get>(h, xp);
+      float* vo = vbase + (t0l * tl1 + t1) * tl2 + t2 + (int64_t)xi0 * (A * A) * pstride;
+#pragma unroll
+      for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
+    }
+    return;
+  } else {
 
   // ---- 2./3. work items (xi_0, tile), tile fastest
-  const int ntile = nt0 * g.R;
-  constexpr int NX = N >= 3 ? A : 1;  // work items per tile (one per xi_0 when N >= 3)
-  const int64_t pstride = (int64_t)g.C * g.T_s;
-  const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;  // V row of the slab's first tile
-  float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
-  for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
-    const int xi0 = w / ntile;
-    const int tl = w - xi0 * ntile;
-    // local tile -> slab offset of its window
-    int rem = tl, base = 0;
+    const int ntile = nt0 * g.R;
+    constexpr int NX = N >= 3 ? A : 1;  // work items per tile (one per xi_0 when N >= 3)
+    const int64_t pstride = (int64_t)g.C * g.T_s;
+    const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;  // V row of the slab's first tile
+    float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
+    for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
+      const int xi0 = w / ntile;
+      const int tl = w - xi0 * ntile;
+      // local tile -> slab offset of its window
+      int rem = tl, base = 0;
 #pragma unroll
-    for (int ax = N - 1; ax >= 1; --ax) {
-      const int ti = rem % g.tiles[ax];
-      rem /= g.tiles[ax];
-      base += ti * M * g.sst[ax];
+      for (int ax = N - 1; ax >= 1; --ax) {
+        const int ti = rem % g.tiles[ax];
+        rem /= g.tiles[ax];
+        base += ti * M * g.sst[ax];
+      }
+      base += rem * M * g.sst[0];
+      in_dispatch<N, A, M, Tab, D>(xi0, S, base, g, xp, vbase + tl, pstride);
     }
-    base += rem * M * g.sst[0];
-    in_dispatch<N, A, M, Tab, D>(xi0, S, base, g, xp, vbase + tl, pstride);
+  }
+}
+
+// One work item = one (b, c) plane slab (tiles [a0, a0 + bt0) of axis 0).
+// Persistent: CTA i handles planes i, i + G, ...; with kTma the slab of the
+// next plane is prefetched into the second slot while the current one is
+// transformed (g.nslot = 2), hiding the TMA latency behind the compute.
+// kTma (N >= 2): slab via one TMA box starting D columns left of -P_last.
+// !kTma: cp.async fallback, D == 0, one slot.
+template <int N, int A, int M, class Tab, int D, bool kTma>
+__global__ void __launch_bounds__(256)
+k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
+              const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm, int nslab) {
+  extern __shared__ __align__(128) float smem_f[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int slab_f = g.slot_bytes / 4;  // slot stride: 128-byte aligned TMA destinations
+  float* H = smem_f + g.nslot * slab_f;
+  const int nwork = nslab * g.C;
+  auto plane = [&](int w, int& b, int& a0, int& nt0, int& c) {
+    const int64_t slab = g.s_beg + w % nslab;
+    c = w / nslab;
+    b = (int)(slab / g.nbox0);
+    const int box = (int)(slab - (int64_t)b * g.nbox0);
+    a0 = box * g.bt0;
+    nt0 = min(g.bt0, g.tiles[0] - a0);
+  };
+  pdl_wait();      // x may come from the preceding kernel; V is read by the previous GEMM
+  pdl_trigger();
+  if constexpr (kTma) {
+    static_assert(N >= 2, "TMA slab path needs N >= 2");
+    const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if ((int)blockIdx.x < nwork) {
+        int b, a0, nt0, c;
+        plane(blockIdx.x, b, a0, nt0, c);
+        issue_slab_tma<N, M, D>(smem_f, &tm, g, b, a0, c, mb0);
+      }
+    }
+    __syncthreads();
+    uint32_t ph = 0;  // bit s: phase of slot s
+    int it = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
+      const int cur = g.nslot == 2 ? (it & 1) : 0;
+      const int wn = w + gridDim.x;
+      if (g.nslot == 2 && threadIdx.x == 0 && wn < nwork) {
+        // the other slot's last reader finished before the previous iteration's trailing barrier
+        int b, a0, nt0, c;
+        plane(wn, b, a0, nt0, c);
+        issue_slab_tma<N, M, D>(smem_f + (cur ^ 1) * slab_f, &tm, g, b, a0, c, mb0 + 8u * (cur ^ 1));
+      }
+      const uint32_t mbc = mb0 + 8u * cur;
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(mbc), "r"((ph >> cur) & 1u)
+            : "memory");
+      }
+      ph ^= 1u << cur;
+      int b, a0, nt0, c;
+      plane(w, b, a0, nt0, c);
+      transform_plane<N, A, M, Tab, D>(smem_f + cur * slab_f, H, V, g, xp, b, a0, nt0, c);
+      __syncthreads();
+      if (g.nslot == 1 && threadIdx.x == 0 && wn < nwork) {
+        int b2, a2, nt2, c2;
+        plane(wn, b2, a2, nt2, c2);
+        issue_slab_tma<N, M, D>(smem_f, &tm, g, b2, a2, c2, mb0);
+      }
+    }
+  } else {
+    static_assert(D == 0, "the cp.async slab path is unshifted");
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int b, a0, nt0, c;
+      plane(w, b, a0, nt0, c);
+      load_slab_cpasync<N, A, M>(smem_f, x, g, b, a0, nt0, c);
+      __syncthreads();
+      transform_plane<N, A, M, Tab, 0>(smem_f, H, V, g, xp, b, a0, nt0, c);
+      __syncthreads();
+    }
   }
 }
 
@@ -266,27 +384,49 @@ inline cudaError_t set_smem(K kern, int bytes) {
 // slab (g.dL is its column shift, 0 or 3); kAllowTma = false compiles only the
 // fallback (run-time tables).
 // Slabs [g.s_beg, g.s_beg + nslab) of the flattened (b, box) order.
+// CTAs per SM of one instantiation at `smem` bytes (cached per instantiation).
+template <class K>
+inline int occupancy(K kern, int smem) {
+  static int cached_smem = -1, cached = 1;
+  if (cached_smem != smem) {
+    int n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, smem) != cudaSuccess || n < 1) n = 1;
+    cached = n;
+    cached_smem = smem;
+  }
+  return cached;
+}
+
+template <class K>
+inline cudaError_t launch_in_kern(K kern, const float* x, float* V, const KGeom& g, const XfParams& xp,
+                                  const CUtensorMap& tm, int nslab, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = set_smem(kern, g.smem_bytes)) != cudaSuccess) return e;
+  const long long nwork = (long long)nslab * g.C;
+  long long grid = nwork;
+  if (g.nslot == 2) {  // persistent: enough CTAs to fill the SMs, each prefetching its next plane
+    static int sms = 0;
+    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+    const long long cap = (long long)occupancy(kern, g.smem_bytes) * sms;
+    if (grid > cap) grid = cap;
+  }
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(256), g.smem_bytes, s, x, V, g, xp, tm, nslab);
+}
+
+// Launch one (N, alpha, m, table) instantiation over slabs [g.s_beg,
+// g.s_beg + nslab).  tm != NULL selects the TMA slab (g.dL is its column
+// shift, 0 or 3); kAllowTma = false compiles only the fallback (run-time tables).
 template <int N, int A, int M, class Tab, bool kAllowTma>
 cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& xp, const CUtensorMap* tm, int nslab,
                       cudaStream_t s) {
-  dim3 grid((unsigned)nslab, (unsigned)g.C);
-  cudaError_t e;
   if constexpr (kAllowTma && N >= 2) {
-    if (tm && g.dL == 0) {
-      auto kern = k_input_xform<N, A, M, Tab, 0, true>;
-      if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
-      return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, *tm);
-    }
-    if (tm && g.dL == 3) {
-      auto kern = k_input_xform<N, A, M, Tab, 3, true>;
-      if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
-      return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, *tm);
-    }
+    if (tm && g.dL == 0) return launch_in_kern(k_input_xform<N, A, M, Tab, 0, true>, x, V, g, xp, *tm, nslab, s);
+    if (tm && g.dL == 3) return launch_in_kern(k_input_xform<N, A, M, Tab, 3, true>, x, V, g, xp, *tm, nslab, s);
   }
-  auto kern = k_input_xform<N, A, M, Tab, 0, false>;
-  if ((e = set_smem(kern, g.slab_bytes)) != cudaSuccess) return e;
+  KGeom g1 = g;
+  g1.nslot = 1;
   CUtensorMap dummy{};
-  return launch_pdl(kern, grid, dim3(256), g.slab_bytes, s, x, V, g, xp, dummy);
+  return launch_in_kern(k_input_xform<N, A, M, Tab, 0, false>, x, V, g1, xp, dummy, nslab, s);
 }
 
 template <int A, int M, class Tab, bool kAllowTma>

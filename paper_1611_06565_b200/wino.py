@@ -190,11 +190,11 @@ def wino_plan_sizes(plan: int):
 
 
 INFO_KEYS = ["N", "m", "r", "alpha", "C", "K", "batch", "T_per_sample", "T_stride", "n_points", "K_stride",
-             "gemm_mode", "fuse", "n_blk", "k_chunk", "chunk_slabs"]
+             "gemm_mode", "fuse", "n_blk", "k_chunk", "chunk_slabs", "gemm_variant", "in_slab_tiles"]
 
 
 def wino_plan_info(plan: int) -> dict:
-    info = (ctypes.c_int64 * 16)()
+    info = (ctypes.c_int64 * len(INFO_KEYS))()
     _check(lib().wino_plan_info(plan, info))
     return dict(zip(INFO_KEYS, list(info)))
 

@@ -205,19 +205,6 @@ def test_input_cp_async_fallback_matches_tma(name, monkeypatch):
     assert torch.equal(y_tma, y_cp)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
-def test_gemm_resident_matches_streaming(name, monkeypatch):
-    # the U-resident GEMM schedule and the streaming one issue the same MMAs
-    # in the same order per output tile: identical bits
-    cfg = SMALL[name]
-    x, g, y_str, plan = run(cfg)
-    plan.close()
-    monkeypatch.setenv("WINO_GEMM_RES", "1")
-    _, _, y_res, plan = run(cfg)
-    plan.close()
-    assert torch.equal(y_res, y_str)
-
-
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 @pytest.mark.parametrize("chunk_mb", ["0.05", "1"])
 def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
@@ -233,14 +220,40 @@ def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
     assert torch.equal(y0, y1), "chunk_slabs=%d" % chunks
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
-def test_gemm_tmem_a_matches_smem_a(name, monkeypatch):
-    # A operand (V_hi / V_lo) from TMEM (k_gemm_ts) vs from shared memory
-    # (k_gemm_tc): the same tf32 products in the same order -> identical bits
+def _run_env(cfg, monkeypatch, **env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, _, y, plan = run(cfg)
+    info = plan.info
+    plan.close()
+    for k in env:
+        monkeypatch.delenv(k)
+    return y, info
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_gemm_variants_bit_identical(name, monkeypatch):
+    # the GEMM variants -- A operand from shared memory (0), from TMEM (1),
+    # CTA pairs with cta_group::2 (2), U resident or streamed -- issue the same
+    # tf32 products in the same order for every output row: identical bits,
+    # so the plan's timing-based choice never changes results
     cfg = SMALL[name]
-    x, g, y_ts, plan = run(cfg)
-    plan.close()
-    monkeypatch.setenv("WINO_GEMM_TS", "0")
-    _, _, y_ss, plan = run(cfg)
-    plan.close()
-    assert torch.equal(y_ts, y_ss)
+    y_ss, _ = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="0")
+    y_res, _ = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="0", WINO_GEMM_RES="1")
+    assert torch.equal(y_ss, y_res)
+    y_ts, info = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="1")
+    assert torch.equal(y_ss, y_ts)
+    if info["gemm_variant"] == 1:
+        y_tsr, _ = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="1", WINO_GEMM_RES="1")
+        assert torch.equal(y_ss, y_tsr)
+    y_pair, info = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="2")
+    assert torch.equal(y_ss, y_pair)
+    _, info = _run_env(cfg, monkeypatch)
+    assert info["gemm_variant"] in (0, 1, 2)
+
+
+def test_gemm_pair_variant_is_exercised(monkeypatch):
+    # c2 / c3 shapes support the CTA-pair kernel (BN = 128): forcing it runs it
+    cfg = SMALL["c3"]
+    _, info = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="2")
+    assert info["gemm_variant"] == 2
