@@ -73,6 +73,9 @@ enum {
   WINO_GEMM_3XTF32 = 3  /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, TMEM fp32 accumulators */
 };
 
+/* Activation f of Eq. (2) for wino_forward_ex. */
+enum { WINO_ACT_NONE = 0, WINO_ACT_RELU = 1 };
+
 /* Fusion bitmask (plan_create_ex `fuse`). */
 enum {
   WINO_FUSE_NONE = 0,
@@ -119,6 +122,15 @@ WINO_API wino_status wino_filter_transform(wino_plan_t plan, const float* g, win
  * [B][C][in...], y: device [B][K][out...], 1 <= B <= planned batch.
  * WINO_ERR_STATE if no filter transform (or mark_ready) happened. */
 WINO_API wino_status wino_forward(wino_plan_t plan, const float* x, float* y, int B, wino_stream_t stream);
+
+/* The full layer of Eq. (2), d' = f(b + conv):
+ *   bias        device [K] fp32 per-output-channel bias b, or NULL (b = 0)
+ *   activation  WINO_ACT_NONE (f = identity) or WINO_ACT_RELU (f = max(., 0))
+ * applied in the spatial domain inside the output transform (a4), after A^T
+ * (SURVEY NEXT-2); otherwise identical to wino_forward (which is
+ * wino_forward_ex(plan, x, y, B, NULL, WINO_ACT_NONE, stream)). */
+WINO_API wino_status wino_forward_ex(wino_plan_t plan, const float* x, float* y, int B, const float* bias,
+                                     int activation, wino_stream_t stream);
 
 /* End-to-end variant with HOST buffers x_host (B x C x in...) and y_host
  * (B x K x out...).  The batch is split into up to 8 sample chunks pipelined

@@ -41,6 +41,8 @@ struct KGeom {
   int64_t s_beg;             // first input slab (b * nbox0 + box) of this launch
   int C, K;
   int m;                     // output tile length (runtime copy)
+  const float* bias;         // optional per-output-channel bias b[k] of Eq. (2) (NULL = none)
+  int act;                   // activation f of Eq. (2): 0 identity, 1 ReLU
   // Input-transform slab (xform_in.cu, plan_input_slab): one CTA stages, for
   // one (b, c) plane, the input needed by tiles [a, a + bt0) along axis 0 and
   // every tile along axes 1..N-1 (a contiguous run of t), zero padded.

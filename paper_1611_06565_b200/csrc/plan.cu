@@ -431,8 +431,11 @@ struct ProfScope {
   cudaError_t end() { return cudaEventRecord(e, s); }
 };
 
-static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, cudaStream_t s) {
+static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, cudaStream_t s,
+                                const float* bias = nullptr, int act = 0) {
   KGeom g = p->geom;
+  g.bias = bias;
+  g.act = act;
   const bool rec = p->prof && p->prof_calls < kMaxProf;
   // TMA map of x, re-encoded when the input pointer or batch changes
   if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
@@ -471,13 +474,20 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
   return WINO_OK;
 }
 
-wino_status wino_forward(wino_plan_t p, const float* x, float* y, int B, wino_stream_t stream) {
+wino_status wino_forward_ex(wino_plan_t p, const float* x, float* y, int B, const float* bias, int activation,
+                            wino_stream_t stream) {
   if (!p || !x || !y) return fail(WINO_ERR_ARG, "NULL plan, x or y");
   if (B < 1 || B > p->batch) return fail(WINO_ERR_ARG, "B=%d outside 1..%d (planned batch)", B, p->batch);
+  if (activation != WINO_ACT_NONE && activation != WINO_ACT_RELU)
+    return fail(WINO_ERR_ARG, "unknown activation %d", activation);
   if (!p->filter_ready) return fail(WINO_ERR_STATE, "forward before wino_filter_transform / mark_ready");
   DeviceGuard guard(p->device);
   CUDA_TRY(cudaGetLastError());
-  return forward_impl(p, x, y, B, (cudaStream_t)stream);
+  return forward_impl(p, x, y, B, (cudaStream_t)stream, bias, activation);
+}
+
+wino_status wino_forward(wino_plan_t p, const float* x, float* y, int B, wino_stream_t stream) {
+  return wino_forward_ex(p, x, y, B, nullptr, WINO_ACT_NONE, stream);
 }
 
 // Host-buffer forward: the batch is split into sample chunks and pipelined

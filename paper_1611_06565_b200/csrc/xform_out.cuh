@@ -51,6 +51,15 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
         o[o1 * M1 + rr] = fmaf(av, v[digits_to_base(rr, N - 1, M, A)], o[o1 * M1 + rr]);
     }
   }
+  // Eq. (2) epilogue in the spatial domain: d' = f(b + conv)
+  if (g.bias || g.act) {
+    const float bk = g.bias ? __ldg(g.bias + k) : 0.f;
+#pragma unroll
+    for (int j = 0; j < MN; ++j) {
+      const float v = o[j] + bk;
+      o[j] = g.act == 1 ? fmaxf(v, 0.f) : v;
+    }
+  }
   // scatter: tile t -> (b, t_1..t_N) (32-bit: T < 2^31 is enforced at plan
   // creation); outputs past `out` are discarded
   int rem = (int)t;

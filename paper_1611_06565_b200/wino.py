@@ -28,9 +28,10 @@ STATUS_NAMES = {0: "WINO_OK", 1: "WINO_ERR_ARG", 2: "WINO_ERR_SHAPE", 3: "WINO_E
                 7: "WINO_ERR_CUDA", 8: "WINO_ERR_NOMEM"}
 WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32 = 0, 1, 2, 3
 WINO_FUSE_NONE, WINO_FUSE_L2_CHUNK = 0, 4
+WINO_ACT_NONE, WINO_ACT_RELU = 0, 1
 
 EXPORTS = ["wino_plan_create", "wino_plan_create_ex", "wino_plan_destroy", "wino_filter_transform",
-           "wino_forward", "wino_forward_host", "wino_plan_out_dims", "wino_plan_sizes",
+           "wino_forward", "wino_forward_ex", "wino_forward_host", "wino_plan_out_dims", "wino_plan_sizes",
            "wino_plan_info", "wino_filter_buffer", "wino_filter_mark_ready", "wino_workspace",
            "wino_profile_enable", "wino_profile_read", "wino_synthesize", "wino_get_transforms",
            "wino_last_error", "wino_version"]
@@ -63,6 +64,7 @@ def lib() -> ctypes.CDLL:
             "wino_plan_destroy": [vp],
             "wino_filter_transform": [vp, vp, vp],
             "wino_forward": [vp, vp, vp, c_int, vp],
+            "wino_forward_ex": [vp, vp, vp, c_int, vp, c_int, vp],
             "wino_forward_host": [vp, vp, vp, c_int, vp],
             "wino_plan_out_dims": [vp, i64p],
             "wino_plan_sizes": [vp, szp, szp],
@@ -168,6 +170,13 @@ def wino_forward(plan: int, x, y, B: int, stream=None) -> None:
     _check(lib().wino_forward(plan, _dev_ptr(x, "x"), _dev_ptr(y, "y"), int(B), _stream_ptr(stream)))
 
 
+def wino_forward_ex(plan: int, x, y, B: int, bias=None, activation: int = WINO_ACT_NONE, stream=None) -> None:
+    """Eq. (2) with bias b[k] (CUDA float32 [K] or None) and activation f."""
+    bp = None if bias is None else _dev_ptr(bias, "bias")
+    _check(lib().wino_forward_ex(plan, _dev_ptr(x, "x"), _dev_ptr(y, "y"), int(B), bp, int(activation),
+                                 _stream_ptr(stream)))
+
+
 def wino_forward_host(plan: int, x_host, y_host, B: int, stream=None) -> None:
     """x_host / y_host: CPU float32 contiguous tensors (pin_memory() for speed)."""
     import torch
@@ -264,12 +273,16 @@ class Plan:
     def filter_transform(self, g, stream=None) -> None:
         wino_filter_transform(self.h, g, stream)
 
-    def forward(self, x, y=None, stream=None):
+    def forward(self, x, y=None, stream=None, bias=None, relu=False):
+        """y = conv(x) (+ bias[k]) (then ReLU): Eq. (2) with b and f optional."""
         import torch
         B = x.shape[0]
         if y is None:
             y = torch.empty((B, self.K) + tuple(self.out_dims), device=x.device, dtype=torch.float32)
-        wino_forward(self.h, x, y, B, stream)
+        if bias is None and not relu:
+            wino_forward(self.h, x, y, B, stream)
+        else:
+            wino_forward_ex(self.h, x, y, B, bias, WINO_ACT_RELU if relu else WINO_ACT_NONE, stream)
         return y
 
     def forward_host(self, x_host, y_host, stream=None) -> None:

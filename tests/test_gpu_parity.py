@@ -257,3 +257,27 @@ def test_gemm_pair_variant_is_exercised(monkeypatch):
     cfg = SMALL["c3"]
     _, info = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="2")
     assert info["gemm_variant"] == 2
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4"])
+def test_bias_relu_epilogue(name):
+    # Eq. (2) with b and f: y = relu(conv + b[k]), fused
+    # into the output transform; oracle: direct conv + b, then max(., 0)
+    cfg = SMALL[name]
+    x, g, y0, plan = run(cfg)
+    gen = torch.Generator("cpu").manual_seed(7)
+    b = torch.randn(cfg.K, generator=gen, dtype=torch.float32) * 0.1
+    xd = x.cuda()
+    y_b = plan.forward(xd, bias=b.cuda()).cpu()
+    y_br = plan.forward(xd, bias=b.cuda(), relu=True).cpu()
+    y_r = plan.forward(xd, relu=True).cpu()
+    plan.close()
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad)
+    bb = b.double().numpy().reshape((1, cfg.K) + (1,) * cfg.N)
+    tl, tm = tolerance(cfg)
+    for y, r in ((y_b, ref + bb), (y_br, np.maximum(ref + bb, 0)), (y_r, np.maximum(ref, 0))):
+        rel, mx = errs(y.numpy(), r)
+        assert rel <= tl and mx <= tm
+    # the epilogue is exact arithmetic on the plain result
+    assert torch.equal(y_r, y0.clamp_min(0))
+    assert torch.equal(y_b, y0 + b.reshape((1, cfg.K) + (1,) * cfg.N))
