@@ -285,7 +285,8 @@ def cfg_dict(cfg, B, world, scaling, fuse=0):
             "F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "per_gpu_batch": B,
             "global_batch": B * world if scaling == "weak" else cfg.batch, "seq_len": None,
             "parallelism": "dp%d (batch shards, U broadcast once)" % world,
-            "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate)",
+            "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate); variant timed at plan creation "
+                    "(0 SMEM-A, 1 TMEM-A, 2 CTA-pair cta_group::2)",
             "pipeline": "L2-chunked a2->a3->a4" if fuse & 4 else "three kernels, V/M via HBM",
             "l2": "flushed: 256 MiB memset between timed steps, outside the per-step events"}
 
@@ -341,7 +342,7 @@ def main():
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
-                                                                 "chunk_slabs")}}
+                                                                 "chunk_slabs", "gemm_variant", "in_slab_tiles")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
         if world == 1 and not args.no_cpu_baseline:
