@@ -57,6 +57,7 @@ struct KGeom {
   int slot_bytes;            // slab slot stride (slab_bytes rounded up to 128)
   int hpitch;                // N = 3, alpha >= 6: row pitch of the axis-0 pass buffer H
   int nslot;                 // slab slots: 2 = persistent CTAs prefetching the next plane
+  int in_threads;            // block size of the input kernel (<= 256)
   int smem_bytes;            // dynamic shared memory of the input kernel (nslot slabs + H)
 };
 

@@ -343,7 +343,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 //   MMA:        tcgen05.mma ... [d], [a_tmem], b_desc (A from TMEM).
 // TMEM columns: 2*BN accumulators + 4*kc A stages.
 template <int BN, bool kRes>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsTS, 1)
 k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
           int C, int K, int kc, int three, int nraw, int nbr, int dbg) {
@@ -383,7 +383,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (lane == 0) {
       for (int s = 0; s < nraw; ++s) {
         mbar_init(rfull(s), 1);
-        mbar_init(rempty(s), 128);
+        mbar_init(rempty(s), 256);
       }
       for (int s = 0; s < nbr; ++s) {
         mbar_init(ufull(s), 1);
@@ -394,7 +394,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_init(tempty(a), 128);
       }
       for (int a = 0; a < na; ++a) {
-        mbar_init(afull(a), 128);
+        mbar_init(afull(a), 256);
         mbar_init(aempty(a), 1);
       }
       mbar_init(bfull, 1);
@@ -438,8 +438,12 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int mb = (int)(u % per_xi) % n_mblk;
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(rempty(s), ph ^ 1u);
-          mbar_expect_tx(rfull(s), a_bytes);
-          tma_load_3d(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s));
+          if (dbg & 16) {
+            mbar_arrive(rfull(s));  // dev knob: no V loads
+          } else {
+            mbar_expect_tx(rfull(s), a_bytes);
+            tma_load_3d(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s));
+          }
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
       }
@@ -476,6 +480,11 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           for (int ch = 0; ch < n_chunks; ++ch) {
             mbar_wait(uempty(s), ph ^ 1u);
             const uint32_t st = bres + s * 2 * b_bytes;
+            if (dbg & 8) {  // dev knob: no U loads
+              mbar_arrive(ufull(s));
+              if (++s == nbr) { s = 0; ph ^= 1u; }
+              continue;
+            }
             mbar_expect_tx(ufull(s), (three ? 2u : 1u) * b_bytes);
 #pragma unroll
             for (int gq = 0; gq < BN / 32; ++gq) {
@@ -488,8 +497,9 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (warp-uniform loop, elected lane issues)
       constexpr uint32_t idesc = idesc_tf32_ts<BN>();
+      const int nk = (dbg & 4) ? 0 : kc / 8;
       const uint32_t lbo = (uint32_t)kc * 128u;
       int as = 0, us = 0;
       uint32_t aph = 0, uph = 0, acc = 0, cph = 0;
@@ -516,35 +526,47 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
           uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
           const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
-          for (int j = 0; j < ((dbg & 4) ? 0 : kc / 8); ++j) {
-            const uint32_t accum = (ch | j) != 0;
-            if (three) {
-              tc_mma_tf32_ts(d, a_lo + 8 * j, dbh, idesc, accum);
-              tc_mma_tf32_ts(d, a_hi + 8 * j, dbl, idesc, 1u);
-              tc_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, 1u);
-            } else {
-              tc_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, accum);
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+              if (j < nk) {
+                const uint32_t accum = (ch | j) != 0;
+                if (three) {
+                  tc_mma_tf32_ts(d, a_lo + 8 * j, dbh + 64 * j, idesc, accum);
+                  tc_mma_tf32_ts(d, a_hi + 8 * j, dbl + 64 * j, idesc, 1u);
+                  tc_mma_tf32_ts(d, a_hi + 8 * j, dbh + 64 * j, idesc, 1u);
+                } else {
+                  tc_mma_tf32_ts(d, a_hi + 8 * j, dbh + 64 * j, idesc, accum);
+                }
+              }
             }
-            dbh += 64; dbl += 64;
+            tc_commit(aempty(as));
+            if constexpr (!kRes) tc_commit(uempty(us));
           }
-          tc_commit(aempty(as));
+          __syncwarp();
           if (++as == na) { as = 0; aph ^= 1u; }
           if constexpr (!kRes) {
-            tc_commit(uempty(us));
             if (++us == nbr) { us = 0; uph ^= 1u; }
           }
         }
-        tc_commit(tfull(acc));
+        if (elect_one()) {
+          tc_commit(tfull(acc));
+          if constexpr (kRes) {
+            if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
+          }
+        }
+        __syncwarp();
         acc ^= 1u;
         if (acc == 0) cph ^= 1u;
-        if constexpr (kRes) {
-          if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
-        }
       }
     }
-  } else if (warp < 4) {  // ---------------- converter: raw V row -> TMEM hi / lo
-    const int row = warp * 32 + lane;
-    const uint32_t lane_sel = (uint32_t)(warp * 32) << 16;
+  } else if (warp < 4 || (warp >= 11 && warp < 15)) {  // ---- converter (8 warps): raw V row -> TMEM hi / lo
+    // warps w and w' with w % 4 == w' % 4 own TMEM lane quarter w % 4; the
+    // second group (warps 11-14) converts the upper half of each chunk's channels
+    const int q = warp & 3, grp = warp < 4 ? 0 : 1;
+    const int row = q * 32 + lane;
+    const uint32_t lane_sel = (uint32_t)(q * 32) << 16;
+    const int cg0 = grp * (kc / 8) / 2, cg1 = (grp + 1) * (kc / 8) / 2;
     int rs = 0, as = 0;
     uint32_t rph = 0, aph = 0;
     for (long long u = u_beg; u < u_end; u += u_step) {
@@ -554,7 +576,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tc_fence_after();
         const float* raw = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
         const uint32_t ahi = tmem_base + lane_sel + a_col0 + as * 2 * kc;
-        for (int cg = 0; cg < ((dbg & 2) ? 0 : kc / 8); ++cg) {
+        for (int cg = cg0; cg < ((dbg & 2) ? cg0 : cg1); ++cg) {
           uint32_t hi[8], lo[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -790,13 +812,13 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
 template <int BN>
 static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P,
                              int t_lo, int T, int64_t T_s, int C, int K) {
-  const dim3 gd(grid), bd(tc::kThreads);
+  const dim3 gd(grid), bd(tc::kThreads), bdts(tc::kThreadsTS);
   const long long Ts = T_s;
   if (tg.variant == kGemmTS) {
     if (tg.resident)
-      return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bd, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+      return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bdts, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
                         C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
-    return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bd, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
+    return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bdts, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
                       C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
   }
   if (tg.resident)

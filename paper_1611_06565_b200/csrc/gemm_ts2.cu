@@ -17,8 +17,8 @@
 //     multicast::cluster); the peer signals readiness to the leader's
 //     mbarriers through shared::cluster addresses (mapa), and its U TMA
 //     completes on the leader's barrier (cp.async.bulk.tensor.cta_group::2).
-// Warps per CTA: 0-3 converter, 4-7 epilogue, 8 V producer, 9 MMA issuer
-// (leader) / TMEM owner, 10 U producer.
+// Warps per CTA: 0-3 and 11-14 converter, 4-7 epilogue, 8 V producer, 9 MMA
+// issuer (leader) / TMEM owner, 10 U producer.
 #include <cstdio>
 #include <cstdlib>
 
@@ -94,7 +94,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32_pair() {
 }
 
 template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
 k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
            const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
            int C, int K, int kc, int three, int nraw, int nbr, int dbg) {
@@ -134,7 +134,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     if (lane == 0) {
       for (int s = 0; s < nraw; ++s) {
         mbar_init(rfull(s), 1);
-        mbar_init(rempty(s), 128);
+        mbar_init(rempty(s), 256);
       }
       for (int s = 0; s < nbr; ++s) {
         mbar_init(ufull(s), 1);    // leader: expect_tx of both halves
@@ -179,8 +179,12 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         const int row0 = t_lo + mp * 2 * BM + (int)rank * BM;
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(rempty(s), ph ^ 1u);
-          mbar_expect_tx(rfull(s), a_bytes);
-          tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * kc, xi, rfull(s));
+          if (dbg & 16) {
+            mbar_arrive(rfull(s));  // dev knob: no V loads
+          } else {
+            mbar_expect_tx(rfull(s), a_bytes);
+            tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * kc, xi, rfull(s));
+          }
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
       }
@@ -198,6 +202,11 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           mbar_wait(uempty(s), ph ^ 1u);
           const uint32_t st = ub0 + s * 2 * hb_bytes;
           const uint32_t lb = mapa(ufull(s), 0);
+          if (dbg & 8) {  // dev knob: no U loads
+            if (leader) mbar_arrive(ufull(s));
+            if (++s == nbr) { s = 0; ph ^= 1u; }
+            continue;
+          }
           if (leader) mbar_expect_tx(ufull(s), 2u * half_tx);
 #pragma unroll
           for (int gq = 0; gq < HN / 32; ++gq) {
@@ -209,8 +218,9 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       }
     }
   } else if (warp == 9) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader CTA)
+    if (leader) {  // ---------------- MMA issuer (leader CTA; warp-uniform loop, elected lane issues)
       constexpr uint32_t idesc = idesc_tf32_pair<BN>();
+      const int nk = (dbg & 4) ? 0 : kc / 8;
       const uint32_t lbo = (uint32_t)kc * 128u;
       int as = 0, us = 0;
       uint32_t aph = 0, uph = 0, acc = 0, cph = 0;
@@ -225,30 +235,40 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           const uint32_t b_hi = ub0 + us * 2 * hb_bytes;
           uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_hi + hb_bytes, lbo, 512u);
           const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
-          for (int j = 0; j < ((dbg & 4) ? 0 : kc / 8); ++j) {
-            const uint32_t accum = (ch | j) != 0;
-            if (three) {
-              tc2_mma_tf32_ts(d, a_lo + 8 * j, dbh, idesc, accum);
-              tc2_mma_tf32_ts(d, a_hi + 8 * j, dbl, idesc, 1u);
-              tc2_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, 1u);
-            } else {
-              tc2_mma_tf32_ts(d, a_hi + 8 * j, dbh, idesc, accum);
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+              if (j < nk) {
+                const uint32_t accum = (ch | j) != 0;
+                if (three) {
+                  tc2_mma_tf32_ts(d, a_lo + 8 * j, dbh + 64 * j, idesc, accum);
+                  tc2_mma_tf32_ts(d, a_hi + 8 * j, dbl + 64 * j, idesc, 1u);
+                  tc2_mma_tf32_ts(d, a_hi + 8 * j, dbh + 64 * j, idesc, 1u);
+                } else {
+                  tc2_mma_tf32_ts(d, a_hi + 8 * j, dbh + 64 * j, idesc, accum);
+                }
+              }
             }
-            dbh += 64; dbl += 64;
+            tc2_commit_mc(aempty(as));
+            tc2_commit_mc(uempty(us));
           }
-          tc2_commit_mc(aempty(as));
-          tc2_commit_mc(uempty(us));
+          __syncwarp();
           if (++as == na) { as = 0; aph ^= 1u; }
           if (++us == nbr) { us = 0; uph ^= 1u; }
         }
-        tc2_commit_mc(tfull(acc));
+        if (elect_one()) tc2_commit_mc(tfull(acc));
+        __syncwarp();
         acc ^= 1u;
         if (acc == 0) cph ^= 1u;
       }
     }
-  } else if (warp < 4) {  // ---------------- converter: raw V row -> own TMEM hi / lo
-    const int row = warp * 32 + lane;
-    const uint32_t lane_sel = (uint32_t)(warp * 32) << 16;
+  } else if (warp < 4 || (warp >= 11 && warp < 15)) {  // ---- converter (8 warps): raw V row -> own TMEM hi / lo
+    // warps w and w' with w % 4 == w' % 4 own TMEM lane quarter w % 4; the
+    // second group (warps 11-14) converts the upper half of each chunk's channels
+    const int q = warp & 3, grp = warp < 4 ? 0 : 1;
+    const int row = q * 32 + lane;
+    const uint32_t lane_sel = (uint32_t)(q * 32) << 16;
+    const int cg0 = grp * (kc / 8) / 2, cg1 = (grp + 1) * (kc / 8) / 2;
     
     int rs = 0, as = 0;
     uint32_t rph = 0, aph = 0;
@@ -259,7 +279,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         tc_fence_after();
         const float* rawp = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
         const uint32_t ahi = tmem_base + lane_sel + a_col0 + as * 2 * kc;
-        for (int cg = 0; cg < kc / 8; ++cg) {
+        for (int cg = cg0; cg < cg1; ++cg) {
           uint32_t hi[8], lo[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -274,7 +294,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         mbar_arrive(rempty(rs));
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (threadIdx.x == 0) mbar_arrive_cluster(mapa(afull(as), 0));
         if (++rs == nraw) { rs = 0; rph ^= 1u; }
         if (++as == na) { as = 0; aph ^= 1u; }
@@ -380,7 +400,7 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
   if (max_pairs_smem != smem) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(num_sms);
-    cfg.blockDim = dim3(tc::kThreads);
+    cfg.blockDim = dim3(tc::kThreadsTS);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -401,7 +421,7 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
   if (pairs > units) pairs = units;
   if (pairs < 1) return cudaSuccess;
   const long long Ts = T_s;
-  return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreads), smem, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P,
+  return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P,
                     t_lo, T, Ts, C, K, tg.kc, tg.three, nraw, nbr, tg.dbg);
 }
 

@@ -11,7 +11,8 @@ namespace wino {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kThreads = 352;
+constexpr int kThreads = 352;    // SS kernel: 4 converter, 4 epilogue, 3 single-thread roles
+constexpr int kThreadsTS = 480;  // TS kernels: + 4 more converter warps (11-14)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -44,6 +45,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm,
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+// One lane of the (fully active) warp: lane 0.  The MMA issuer runs its loop
+// in the whole warp so loop state stays warp-uniform (uniform registers feed
+// UTCHMMA directly); only the elected lane issues tcgen05.mma / commit.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+  return p != 0;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

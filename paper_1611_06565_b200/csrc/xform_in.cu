@@ -68,6 +68,8 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
   g.nbox0 = (g.tiles[0] + bt0 - 1) / bt0;
   g.e[0] = bt0 * m + halo;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
+  g.in_threads = 256;
+  if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256)
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(nslot * g.slot_bytes + hbytes(bt0));

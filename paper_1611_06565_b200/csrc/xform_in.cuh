@@ -386,11 +386,11 @@ inline cudaError_t set_smem(K kern, int bytes) {
 // Slabs [g.s_beg, g.s_beg + nslab) of the flattened (b, box) order.
 // CTAs per SM of one instantiation at `smem` bytes (cached per instantiation).
 template <class K>
-inline int occupancy(K kern, int smem) {
+inline int occupancy(K kern, int smem, int threads) {
   static int cached_smem = -1, cached = 1;
   if (cached_smem != smem) {
     int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, smem) != cudaSuccess || n < 1) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess || n < 1) n = 1;
     cached = n;
     cached_smem = smem;
   }
@@ -407,10 +407,10 @@ inline cudaError_t launch_in_kern(K kern, const float* x, float* V, const KGeom&
   if (g.nslot == 2) {  // persistent: enough CTAs to fill the SMs, each prefetching its next plane
     static int sms = 0;
     if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
-    const long long cap = (long long)occupancy(kern, g.smem_bytes) * sms;
+    const long long cap = (long long)occupancy(kern, g.smem_bytes, g.in_threads) * sms;
     if (grid > cap) grid = cap;
   }
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(256), g.smem_bytes, s, x, V, g, xp, tm, nslab);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(g.in_threads), g.smem_bytes, s, x, V, g, xp, tm, nslab);
 }
 
 // Launch one (N, alpha, m, table) instantiation over slabs [g.s_beg,
