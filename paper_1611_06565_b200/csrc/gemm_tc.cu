@@ -193,7 +193,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (warp-uniform loop, elected lane issues)
       constexpr uint32_t idesc = idesc_tf32<BN>();
       const uint32_t lbo = (uint32_t)kc * 128u;
       int s = 0, us = 0;
@@ -221,33 +221,43 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t b_hi = kRes ? bres + ch * b_bytes : bres + us * 2 * b_bytes;
           const uint32_t b_lo = kRes ? bres + (n_chunks + ch) * b_bytes : b_hi + b_bytes;
           // descriptors of k-step 0; k-step j is +j*1024 B = +64 in the address field
-          uint64_t dah = sdesc(st, lbo, 512u), dal = sdesc(st + a_bytes, lbo, 512u);
-          uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
-          for (int j = 0; j < kc / 8; ++j) {
-            const uint32_t accum = (ch | j) != 0;
-            if (three) {
-              tc_mma_tf32(d, dal, dbh, idesc, accum);
-              tc_mma_tf32(d, dah, dbl, idesc, 1u);
-              tc_mma_tf32(d, dah, dbh, idesc, 1u);
-            } else {
-              tc_mma_tf32(d, dah, dbh, idesc, accum);
+          const uint64_t dah = sdesc(st, lbo, 512u), dal = sdesc(st + a_bytes, lbo, 512u);
+          const uint64_t dbh = sdesc(b_hi, lbo, 512u), dbl = sdesc(b_lo, lbo, 512u);
+          const int nk = kc / 8;
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+              if (j < nk) {
+                const uint32_t accum = (ch | j) != 0;
+                const uint64_t o = 64ull * j;
+                if (three) {
+                  tc_mma_tf32(d, dal + o, dbh + o, idesc, accum);
+                  tc_mma_tf32(d, dah + o, dbl + o, idesc, 1u);
+                  tc_mma_tf32(d, dah + o, dbh + o, idesc, 1u);
+                } else {
+                  tc_mma_tf32(d, dah + o, dbh + o, idesc, accum);
+                }
+              }
             }
-            dah += 64; dal += 64; dbh += 64; dbl += 64;
+            tc_commit(oempty(s));
+            if constexpr (!kRes) tc_commit(uempty(us));
           }
-          tc_commit(oempty(s));
+          __syncwarp();
           if (++s == nop) { s = 0; ph ^= 1u; }
           if constexpr (!kRes) {
-            tc_commit(uempty(us));
             if (++us == nbr) { us = 0; uph ^= 1u; }
           }
         }
-        tc_commit(tfull(acc));
+        if (elect_one()) {
+          tc_commit(tfull(acc));
+          // release the resident U block after its last unit
+          if constexpr (kRes) {
+            if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
+          }
+        }
+        __syncwarp();
         acc ^= 1u;
         if (acc == 0) aph ^= 1u;
-        if constexpr (kRes) {
-          // release the resident U block after its last unit
-          if (u + 1 >= u_end || (u + 1) / n_mblk != cur_pair) tc_commit(bempty);
-        }
       }
     }
   } else if (warp < 4) {  // ---------------- converter (128 threads): raw -> hi, lo
