@@ -771,43 +771,22 @@ static TcSmem plan_smem(const TcGemm& tg, int C) {
   return tg.variant == kGemmTS ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
 }
 
-cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P, int64_t T_s,
-                            int C, int K_s, int K, int three, int device) {
-  tg.ready = false;
-  tg.bn = pick_bn(K);
-  tg.kc = C >= 32 ? 32 : ((C + 7) / 8) * 8;
-  if (const char* ev = getenv("WINO_GEMM_KC")) tg.kc = atoi(ev);  // dev knob (8, 16, 32)
-  tg.three = three;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  tg.num_sms = sms;
+// Capabilities and shared-memory attributes for N tile `bn` (tg.kc, tg.resident set).
+static cudaError_t prep_bn(TcGemm& tg, int bn, int C) {
+  tg.bn = bn;
   // TS mode (A in TMEM) when the accumulators and two A stages fit in TMEM;
   // CTA pairs (cta_group::2) on top of TS
-  tg.can_ts = 2 * tg.bn + 4 * tg.kc <= 512;
-  tg.can_pair = tg.can_ts && ts2_supported(tg.bn, tg.kc);
-  tg.variant = tg.can_ts ? kGemmTS : kGemmSS;
-  // U streamed through its ring by default: the grid-strided unit order keeps
-  // the CTAs on neighbouring m-blocks (DRAM locality), measured faster than
-  // the U-resident contiguous ranges; WINO_GEMM_RES=1 selects U-resident
-  tg.resident = false;
-  if (const char* ev = getenv("WINO_GEMM_RES"))
-    tg.resident = atoi(ev) != 0 && (tg.can_ts ? ts_smem(tg.bn, tg.kc, C, true) : tc_smem(tg.bn, tg.kc, C, true)).nraw >= 4;
-  tg.dbg = 0;  // dev-only experiment knob: 1 no M stores, 2 no V split, 4 no MMAs (results invalid)
-  if (const char* ev = getenv("WINO_GEMM_DBG")) tg.dbg = atoi(ev);
-  cudaError_t e;
-  if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
-  if (tg.can_ts && (e = encode_v_ts(&tg.tmA_ts, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
-  if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
-  if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
+  tg.can_ts = 2 * bn + 4 * tg.kc <= 512;
+  tg.can_pair = tg.can_ts && ts2_supported(bn, tg.kc);
+  cudaError_t e = cudaSuccess;
   for (int ts = 0; ts <= (tg.can_ts ? 1 : 0); ++ts) {
-    const TcSmem sm = ts ? ts_smem(tg.bn, tg.kc, C, tg.resident) : tc_smem(tg.bn, tg.kc, C, tg.resident);
+    const TcSmem sm = ts ? ts_smem(bn, tg.kc, C, tg.resident) : tc_smem(bn, tg.kc, C, tg.resident);
     if (sm.nraw < 1) {
       if (!ts) return cudaErrorInvalidConfiguration;
       tg.can_ts = tg.can_pair = false;
-      tg.variant = kGemmSS;
       break;
     }
-    switch (tg.bn) {
+    switch (bn) {
       case 32: e = set_attr<32>(sm.bytes, tg.resident, ts); break;
       case 64: e = set_attr<64>(sm.bytes, tg.resident, ts); break;
       case 128: e = set_attr<128>(sm.bytes, tg.resident, ts); break;
@@ -815,6 +794,42 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
     }
     if (e != cudaSuccess) return e;
   }
+  tg.variant = tg.can_ts ? kGemmTS : kGemmSS;
+  return cudaSuccess;
+}
+
+cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P, int64_t T_s,
+                            int C, int K_s, int K, int three, int device) {
+  tg.ready = false;
+  tg.bn_max = pick_bn(K);
+  tg.kc = C >= 32 ? 32 : ((C + 7) / 8) * 8;
+  if (const char* ev = getenv("WINO_GEMM_KC")) tg.kc = atoi(ev);  // dev knob (8, 16, 32)
+  tg.three = three;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  tg.num_sms = sms;
+  // U streamed through its ring by default: the grid-strided unit order keeps
+  // the CTAs on neighbouring m-blocks (DRAM locality), measured faster than
+  // the U-resident contiguous ranges; WINO_GEMM_RES=1 selects U-resident
+  tg.resident = false;
+  if (const char* ev = getenv("WINO_GEMM_RES")) {
+    const int bn = tg.bn_max;
+    const bool ts = 2 * bn + 4 * tg.kc <= 512;
+    tg.resident = atoi(ev) != 0 && (ts ? ts_smem(bn, tg.kc, C, true) : tc_smem(bn, tg.kc, C, true)).nraw >= 4;
+  }
+  tg.dbg = 0;  // dev-only experiment knob: 1 no M stores, 2 no V split, 4 no MMAs (results invalid)
+  if (const char* ev = getenv("WINO_GEMM_DBG")) tg.dbg = atoi(ev);
+  cudaError_t e;
+  if ((e = encode3d(&tg.tmA, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
+  if ((e = encode_v_ts(&tg.tmA_ts, V, T_s, C, P, tg.kc)) != cudaSuccess) return e;
+  if ((e = encode3d(&tg.tmBhi, Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
+  if ((e = encode3d(&tg.tmBlo, Ulo ? Ulo : Uhi, K_s, C, P, tg.kc)) != cudaSuccess) return e;
+  int bn = tg.bn_max;
+  if (const char* ev = getenv("WINO_GEMM_BN")) {  // dev knob: smaller N tile (divides K_s)
+    const int b = atoi(ev);
+    if ((b == 32 || b == 64 || b == 128) && b < bn) bn = b;
+  }
+  if ((e = prep_bn(tg, bn, C)) != cudaSuccess) return e;
   tg.ready = true;
   return cudaSuccess;
 }
@@ -860,21 +875,29 @@ cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, i
     if ((v == kGemmTS && tg.can_ts) || (v == kGemmPair && tg.can_pair) || v == kGemmSS) tg.variant = v;
     return cudaSuccess;
   }
-  if (const char* ev = getenv("WINO_GEMM_PAIR"))  // dev knob: pair on/off without timing
-    if (!atoi(ev)) { tg.variant = tg.can_ts ? kGemmTS : kGemmSS; return cudaSuccess; }
-  int cand[3], nc = 0;
-  cand[nc++] = kGemmSS;
-  if (tg.can_ts) cand[nc++] = kGemmTS;
-  if (tg.can_pair) cand[nc++] = kGemmPair;
-  if (nc == 1) { tg.variant = kGemmSS; return cudaSuccess; }
+  if (getenv("WINO_GEMM_BN")) return cudaSuccess;  // dev knob fixes the tile and the default variant
+  // candidates: (N tile, variant); a 256-wide N tile (K > 128) is also tried
+  // at 128, where TMEM has room for A stages and the CTA-pair kernel applies
+  struct Cand { int bn, v; };
+  Cand cand[8];
+  int nc = 0;
+  const int bns[2] = {tg.bn_max, 128};
+  for (int ib = 0; ib < (tg.bn_max == 256 ? 2 : 1); ++ib) {
+    cudaError_t e = prep_bn(tg, bns[ib], C);
+    if (e != cudaSuccess) return e;
+    cand[nc++] = {bns[ib], kGemmSS};
+    if (tg.can_ts) cand[nc++] = {bns[ib], kGemmTS};
+    if (tg.can_pair) cand[nc++] = {bns[ib], kGemmPair};
+  }
   cudaEvent_t e0, e1;
   cudaError_t e;
   if ((e = cudaEventCreate(&e0)) != cudaSuccess) return e;
   if ((e = cudaEventCreate(&e1)) != cudaSuccess) return e;
   float best = 1e30f;
-  int best_v = cand[0];
+  Cand bc = cand[0];
   for (int i = 0; i < nc; ++i) {
-    tg.variant = cand[i];
+    if ((e = prep_bn(tg, cand[i].bn, C)) != cudaSuccess) break;
+    tg.variant = cand[i].v;
     if ((e = launch_gemm_tc(tg, Mo, P, 0, T, T_s, C, K, 0)) != cudaSuccess) break;  // warm-up
     float t = 0.f;
     cudaEventRecord(e0, 0);
@@ -882,13 +905,16 @@ cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, i
     cudaEventRecord(e1, 0);
     if ((e = cudaEventSynchronize(e1)) != cudaSuccess) break;
     cudaEventElapsedTime(&t, e0, e1);
-    if (t < best) { best = t; best_v = cand[i]; }
+    if (t < best) { best = t; bc = cand[i]; }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  tg.variant = best_v;
-  if (getenv("WINO_DEBUG")) fprintf(stderr, "[wino] gemm variant %d (%.4f ms per launch)\n", best_v, best / 3);
-  return e;
+  if (e != cudaSuccess) return e;
+  if ((e = prep_bn(tg, bc.bn, C)) != cudaSuccess) return e;
+  tg.variant = bc.v;
+  if (getenv("WINO_DEBUG"))
+    fprintf(stderr, "[wino] gemm bn %d variant %d (%.4f ms per launch)\n", bc.bn, bc.v, best / 3);
+  return cudaSuccess;
 }
 
 }  // namespace wino

@@ -38,6 +38,7 @@ struct TcGemm {
   CUtensorMap tmBhi;  // U_hi [P][C][K_s]
   CUtensorMap tmBlo;  // U_lo
   int bn;             // N tile (32, 64, 128, 256)
+  int bn_max;         // widest N tile for K (pick_bn)
   int kc;             // channels per pipeline stage (multiple of 8, <= 32)
   int three;          // 1: 3xTF32, 0: 1xTF32
   int num_sms;

@@ -281,3 +281,22 @@ def test_bias_relu_epilogue(name):
     # the epilogue is exact arithmetic on the plain result
     assert torch.equal(y_r, y0.clamp_min(0))
     assert torch.equal(y_b, y0 + b.reshape((1, cfg.K) + (1,) * cfg.N))
+
+
+def test_gemm_n_tile_choice_bit_identical(monkeypatch):
+    # K > 128: the plan also times N tile 128 (where TMEM fits A stages and the
+    # CTA-pair kernel applies) against 256; the tile changes which CTA computes
+    # an output, never its arithmetic
+    from paper_1611_06565_b200.workloads import LayerConfig
+    cfg = LayerConfig("k200", 3, 2, 40, 200, (6, 9, 10), 3, 1, 4, "relu_normal", "he")
+    y256, info = _run_env(cfg, monkeypatch, WINO_GEMM_VARIANT="0")
+    assert info["n_blk"] == 256
+    for v in ("0", "1", "2"):
+        y128, info = _run_env(cfg, monkeypatch, WINO_GEMM_BN="128", WINO_GEMM_VARIANT=v)
+        assert info["n_blk"] == 128
+        assert torch.equal(y256, y128)
+    y, info = _run_env(cfg, monkeypatch)
+    assert torch.equal(y256, y)
+    x, g = make_inputs(cfg)
+    rel, mx = errs(y.numpy(), direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad))
+    assert rel <= 1e-5 and mx <= 1e-3
