@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--extra", default="c3,c4,c5", help="comma list of further configs ('' for none)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--fuse", type=int, default=0, help="plan fuse bitmask (4 = L2-chunked a2->a3->a4)")
+    ap.add_argument("--nets", default="fig4_f54,fig4_f34,fig3_f54",
+                    help="the paper's own 2-D workloads (Figures 3 and 4) to time at N=1 ('' for none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
     return ap.parse_args()
@@ -267,6 +269,61 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
     return results
 
 
+# Figure 4 of the paper: 10.9 MVox/s on 18 cores of a Xeon E7-8890, context only
+PAPER_FIG4_MVOX = 10.9
+
+
+def run_nets(args, local):
+    """The paper's own 2-D workloads (workloads.NETS): each net at each of its
+    batch sizes, device-resident, L2 flushed before every pass, CUDA events
+    around the whole chain of layers.  MVox/s = batch x input voxels / time
+    (reading #16)."""
+    import torch
+    import paper_1611_06565_b200 as pkg
+    from paper_1611_06565_b200.workloads import NETS, make_net_inputs
+    dev = torch.device("cuda", local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sink = torch.empty((), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    steps = max(3, min(args.steps, 20))
+    out = {}
+    for name in [n for n in args.nets.split(",") if n]:
+        net_cfg = NETS[name]
+        rows = {}
+        for B in net_cfg.batches:
+            x, gs = make_net_inputs(net_cfg, seed=0, batch=B)
+            layers = [(l.N, l.dims, l.m, l.r, l.C, l.K, l.padding) for l in net_cfg.layers]
+            net = pkg.Net(layers, B, device=local)
+            net.filter_transform([g.to(dev) for g in gs], stream)
+            xd = x.to(dev)
+            for _ in range(max(args.warmup, 3)):
+                net.forward(xd, stream)
+            torch.cuda.synchronize(dev)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for a, b in evs:
+                flush.zero_()
+                torch.sum(flush.view(torch.int64), dim=0, out=sink)
+                a.record(stream)
+                net.forward(xd, stream)
+                b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+            rows[str(B)] = {"ms_per_pass": round(ms, 4),
+                            "mvox_s": round(B * net_cfg.in_voxels / (ms * 1e-3) / 1e6, 1),
+                            "tflops_direct_equiv": round(net_cfg.direct_flops(B) / (ms * 1e-3) / 1e12, 2),
+                            "gemm_variants": [p.info["gemm_variant"] for p in net.plans]}
+            net.close()
+            del xd
+            torch.cuda.empty_cache()
+        best = max(rows.values(), key=lambda r: r["mvox_s"])
+        out[name] = {"desc": net_cfg.desc, "layers": len(net_cfg.layers),
+                     "F": "F(%d^2,%d^2)" % (net_cfg.layers[0].m, net_cfg.layers[0].r),
+                     "by_batch": rows, "best_mvox_s": best["mvox_s"]}
+        if name.startswith("fig4"):
+            out[name]["paper_mvox_s"] = {"value": PAPER_FIG4_MVOX, "hardware": "18-core Xeon E7-8890 (context only)"}
+    return out
+
+
 def cpu_baseline_sample(cfg, seconds):
     """Time the float64 oracle (as it stands) on a bounded sample of the
     workload: outputs computed one by one at random positions."""
@@ -372,6 +429,8 @@ def main():
         out["filter_transform_ms"] = configs[args.config]["filter_transform_ms"]
         out["stages"] = configs[args.config]["stages"]
         out["configs"] = configs
+        if world == 1 and args.nets:
+            out["paper_workloads"] = run_nets(args, local)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -114,3 +114,60 @@ def make_inputs(cfg: LayerConfig, seed: int = 0, batch: int = None):
 def tolerance(cfg: LayerConfig):
     """(relL2, max-abs / max|y|) bounds of BASELINE.json north_star."""
     return (2e-6, 1e-4) if cfg.m == 2 else (1e-5, 1e-3)
+
+
+# ---------------------------------------------------------------- paper nets
+# The paper's own 2-D measurements (SURVEY.md 8(f) NEXT-1; DESIGN.md reading
+# #16): Figure 4 propagates 224x224 images through three convolution layers of
+# 32 channels and 32 kernels of size 4x4 (PAPER.md:307), at batch 1, 20 and
+# 200, reported in megavoxels per second; Figure 3 is one 4x4 layer on a
+# 1024x1024 image (PAPER.md:294).  Unstated and read here: valid convolution
+# (no padding), C = K = 32 for every layer including Figure 3's, x ~ N(0, 1),
+# g ~ N(0, 2 / (C r^2)).  Transforms: F(5, 4) (Table 1 (c), D = 8, the paper's
+# choice for 4x4 kernels, PAPER.md:281) and F(3, 4) (D = 6).
+@dataclass(frozen=True)
+class NetConfig:
+    name: str
+    layers: Tuple[LayerConfig, ...]
+    batches: Tuple[int, ...]
+    desc: str = ""
+
+    @property
+    def in_voxels(self) -> int:
+        """Input voxels of one sample (the MVox/s numerator, reading #16)."""
+        return math.prod(self.layers[0].dims)
+
+    def direct_flops(self, batch: int) -> int:
+        return sum(l.direct_flops(batch) for l in self.layers)
+
+
+def _chain(name, dims, depth, C, r, m, batches, desc):
+    layers = []
+    for i in range(depth):
+        layers.append(LayerConfig("%s_l%d" % (name, i + 1), len(dims), batches[0], C, C, tuple(dims), r, 0, m,
+                                  "normal", "he"))
+        dims = [d - r + 1 for d in dims]
+    return NetConfig(name, tuple(layers), tuple(batches), desc)
+
+
+NETS = {
+    "fig4_f54": _chain("fig4_f54", [224, 224], 3, 32, 4, 5, (1, 20, 200),
+                       "Figure 4: 224x224 through 3 layers 32->32, 4x4 kernels, F(5x5,4x4) (D=8)"),
+    "fig4_f34": _chain("fig4_f34", [224, 224], 3, 32, 4, 3, (1, 20, 200),
+                       "Figure 4: 224x224 through 3 layers 32->32, 4x4 kernels, F(3x3,4x4) (D=6)"),
+    "fig3_f54": _chain("fig3_f54", [1024, 1024], 1, 32, 4, 5, (1,),
+                       "Figure 3: one 4x4 layer on a 1024x1024 image, 32->32, F(5x5,4x4) (D=8)"),
+}
+
+
+def make_net_inputs(net: NetConfig, seed: int = 0, batch: int = 1):
+    """(x [B][C][dims], [g_1 .. g_L]) as CPU float32 tensors: x first, then
+    each layer's kernels in order, from one seeded generator."""
+    gen = torch.Generator("cpu").manual_seed(seed)
+    l0 = net.layers[0]
+    x = torch.randn((batch, l0.C) + tuple(l0.dims), generator=gen, dtype=torch.float32)
+    gs = []
+    for l in net.layers:
+        gs.append((torch.randn((l.K, l.C) + (l.r,) * l.N, generator=gen, dtype=torch.float32)
+                   * math.sqrt(2.0 / (l.C * l.r ** l.N))).contiguous())
+    return x.contiguous(), gs
