@@ -123,15 +123,11 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ helpers
 def stage_bytes(cfg, B):
-    """Algorithmic (compulsory) bytes of each stage for B samples."""
-    T = cfg.tiles(B)
-    P = cfg.alpha ** cfg.N
-    x = B * cfg.C * math.prod(cfg.dims) * 4
-    y = B * cfg.K * math.prod(cfg.out_dims) * 4
-    V = P * cfg.C * T * 4
-    M = P * cfg.K * T * 4
-    U = P * cfg.C * cfg.K * 4
-    return {"input_xform": x + V, "gemm": V + U + M, "output_xform": M + y}
+    """Algorithmic (compulsory) bytes of each stage for B samples (DESIGN.md
+    Sec. 8), from the package's analytic cost model."""
+    from paper_1611_06565_b200.cost import stage_model
+    st = stage_model(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding)
+    return {s: st[s]["bytes"] for s in ("input_xform", "gemm", "output_xform")}
 
 
 def roofline_for(cfg, B, stage, ms, peaks):
