@@ -34,6 +34,7 @@ import subprocess
 import sys
 import tempfile
 import time
+from dataclasses import replace
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -178,21 +179,27 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
     results = {}
     for name in cfg_names:
         cfg = CONFIGS[name]
+        ksplit = False
         if args.scaling == "weak":
-            B = cfg.batch
+            B, Kl = cfg.batch, cfg.K
             x, g = make_inputs(cfg, seed=rank)
             gref = make_inputs(cfg, seed=0)[1]
             g = gref                                  # same weights on every rank
         else:
-            lo, hi = wdist.shard_range(cfg.batch, rank, world)
-            B = hi - lo
+            # strong: the config batch over the ranks; when the batch is
+            # smaller than the world the output channels split too (NEXT-3)
+            b_lo, b_hi, k_lo, k_hi = wdist.grid_shard(cfg.batch, cfg.K, rank, world)
+            B, Kl = b_hi - b_lo, k_hi - k_lo
+            ksplit = Kl != cfg.K
             xf, g = make_inputs(cfg, seed=0)
-            x = xf[lo:hi].contiguous()
-        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding, device=local, fuse=args.fuse)
+            x = xf[b_lo:b_hi].contiguous()
+            g = g[k_lo:k_hi].contiguous()
+        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, Kl, B, cfg.padding, device=local, fuse=args.fuse)
         stream = torch.cuda.current_stream(dev)
-        # a1 once per weight set on rank 0, U broadcast over NCCL to the others
+        # a1 once per weight set on rank 0, U broadcast over NCCL to the
+        # others; with a K split every rank transforms its own kernel slice
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if rank == 0:
+        if rank == 0 or ksplit:
             gd = g.to(dev)
             e0.record(stream)
             plan.filter_transform(gd, stream)
@@ -201,12 +208,13 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
             filt_ms = e0.elapsed_time(e1)
         else:
             filt_ms = None
-        wdist.broadcast_filter(plan.filter_tensor(), src=0)
+        if not ksplit:
+            wdist.broadcast_filter(plan.filter_tensor(), src=0)
         torch.cuda.synchronize(dev)
-        if rank != 0:
+        if rank != 0 and not ksplit:
             plan.mark_ready()
         xd = x.to(dev)
-        y = torch.empty((B, cfg.K) + cfg.out_dims, device=dev, dtype=torch.float32)
+        y = torch.empty((B, Kl) + cfg.out_dims, device=dev, dtype=torch.float32)
         for _ in range(max(args.warmup, 3)):
             plan.forward(xd, y, stream)
         torch.cuda.synchronize(dev)
@@ -238,7 +246,7 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
         stages = dict(zip(["input_xform", "gemm", "output_xform"], [s / calls for s in stage_ms]))
         # ---- end to end through the public C ABI with host buffers
         xh = x.pin_memory()
-        yh = torch.empty((B, cfg.K) + cfg.out_dims, dtype=torch.float32).pin_memory()
+        yh = torch.empty((B, Kl) + cfg.out_dims, dtype=torch.float32).pin_memory()
         for _ in range(2):
             plan.forward_host(xh, yh, stream)
         wdist.barrier(device=dev)
@@ -250,11 +258,12 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
             b.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = wdist.max_over_ranks(sum(a.elapsed_time(b) for a, b in ee) / len(ee), device=dev)
-        flops_rank = cfg.direct_flops(B)
+        # whole-job flops: weak = world x one config batch; strong = one config batch
+        flops_job = world * cfg.direct_flops(B) if args.scaling == "weak" else cfg.direct_flops()
         res = {
-            "name": name, "cfg": cfg, "B": B, "ms": ms, "tflops": world * flops_rank / (ms * 1e-3) / 1e12,
+            "name": name, "cfg": cfg, "cfg_local": replace(cfg, K=Kl), "B": B, "ms": ms, "tflops": flops_job / (ms * 1e-3) / 1e12, "K_local": Kl,
             "stages_ms": stages, "filter_ms": filt_ms, "e2e_ms": e2e_ms,
-            "e2e_tflops": world * flops_rank / (e2e_ms * 1e-3) / 1e12,
+            "e2e_tflops": flops_job / (e2e_ms * 1e-3) / 1e12,
             "h2d": xh.numel() * 4, "d2h": yh.numel() * 4, "launches": 3 * args.steps,
             "info": plan.info,
         }
@@ -347,11 +356,16 @@ def cpu_baseline_sample(cfg, seconds):
 
 
 def cfg_dict(cfg, B, world, scaling, fuse=0):
+    from paper_1611_06565_b200.dist import grid_shape
+    if scaling == "weak" or cfg.batch >= world:
+        par = "dp%d (batch shards, U broadcast once)" % world
+    else:
+        par = "grid %dx%d (batch shards x output-channel shards, no reduction)" % grid_shape(cfg.batch, cfg.K, world)
     return {"workload": "%s: %s" % (cfg.name, cfg.desc), "model": "N-D Winograd conv layer (synthetic)",
             "N": cfg.N, "dims": list(cfg.dims), "C": cfg.C, "K": cfg.K, "kernel": cfg.r, "pad": cfg.pad,
             "F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "per_gpu_batch": B,
             "global_batch": B * world if scaling == "weak" else cfg.batch, "seq_len": None,
-            "parallelism": "dp%d (batch shards, U broadcast once)" % world,
+            "parallelism": par,
             "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate); variant timed at plan creation "
                     "(0 SMEM-A, 1 TMEM-A, 2 CTA-pair cta_group::2)",
             "pipeline": "L2-chunked a2->a3->a4" if fuse & 4 else "three kernels, V/M via HBM",
@@ -399,13 +413,13 @@ def main():
         for name, r in res.items():
             st = r["stages_ms"]
             dom = max(st, key=st.get)
-            rl = roofline_for(r["cfg"], r["B"], dom, st[dom], peaks)
+            rl = roofline_for(r["cfg_local"], r["B"], dom, st[dom], peaks)
             rl["kernel"] = dom
             tk = traffic.get(name, {}).get(dom)
             if tk is not None:
                 rl["traffic"] = tk
             per_stage = {s: {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
-                         for s, v in st.items() for rf in [roofline_for(r["cfg"], r["B"], s, v, peaks)]}
+                         for s, v in st.items() for rf in [roofline_for(r["cfg_local"], r["B"], s, v, peaks)]}
             configs[name] = {"ms_per_layer": round(r["ms"], 5), "tflops_direct_equiv": round(r["tflops"], 2),
                              "stages": per_stage, "dominant": rl,
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),

@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1611_06565_b200.dist import broadcast_filter, max_over_ranks, shard_range
+from paper_1611_06565_b200.dist import (broadcast_filter, gather_outputs, grid_shape, grid_shard, max_over_ranks,
+                                        shard_range)
 
 
 def _free_port():
@@ -36,7 +37,16 @@ def _worker(rank, world, port, q):
         m = max_over_ranks(1.5 + rank)
         # strong-scaling shards cover the batch exactly once
         lo, hi = shard_range(7, rank, world)
-        q.put((rank, ok_bcast, m, lo, hi))
+        # batch 1 < 2 ranks: output channels split; the gathered shards
+        # rebuild the full y (each rank fills only its own slice)
+        yfull = torch.arange(1 * 5 * 3 * 4, dtype=torch.float32).reshape(1, 5, 3, 4)
+        b0, b1, k0, k1 = grid_shard(1, 5, rank, world)
+        ok_gather = bool(torch.equal(gather_outputs(yfull[b0:b1, k0:k1].clone(), 1, 5), yfull))
+        # batch 3 x K 4 over 2 ranks: batch shards, full K each
+        b0, b1, k0, k1 = grid_shard(3, 4, rank, world)
+        y2 = torch.randn(3, 4, 2, generator=torch.Generator().manual_seed(5))
+        ok_gather2 = bool(torch.equal(gather_outputs(y2[b0:b1, k0:k1].clone(), 3, 4), y2))
+        q.put((rank, ok_bcast, m, lo, hi, ok_gather, ok_gather2))
     finally:
         dist.destroy_process_group()
 
@@ -57,6 +67,26 @@ def test_two_rank_gloo():
     assert all(r[2] == 2.5 for r in res), "max over ranks"
     covered = [i for r in sorted(res, key=lambda r: r[3]) for i in range(r[3], r[4])]
     assert covered == list(range(7))
+    assert all(r[5] and r[6] for r in res), "gather of (batch x K) grid shards"
+
+
+@pytest.mark.parametrize("batch,K,world", [(32, 128, 8), (1, 4, 4), (1, 128, 8), (2, 64, 8), (3, 5, 6), (6, 7, 4)])
+def test_grid_shard_partition(batch, K, world):
+    pb, pk = grid_shape(batch, K, world)
+    assert pb * pk == world and pb <= batch and pk <= K
+    if batch >= world:
+        assert pk == 1                       # batch sharding whenever it suffices
+    cells = []
+    for r in range(world):
+        b0, b1, k0, k1 = grid_shard(batch, K, r, world)
+        assert b1 > b0 and k1 > k0
+        cells += [(b, k) for b in range(b0, b1) for k in range(k0, k1)]
+    assert sorted(cells) == [(b, k) for b in range(batch) for k in range(K)]
+
+
+def test_grid_shape_too_many_ranks():
+    with pytest.raises(ValueError):
+        grid_shape(1, 2, 4)
 
 
 @pytest.mark.parametrize("batch,world", [(32, 1), (32, 8), (7, 3), (1, 2), (16, 4)])
