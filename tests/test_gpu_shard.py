@@ -42,11 +42,10 @@ def _sharded(cfg, x, g, world):
     return y
 
 
-@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 3), ("c3", 4), ("c4", 6), ("c5", 8)])
-def test_grid_shards_equal_single_plan_bitwise(name, world):
+@pytest.mark.parametrize("name,B,world", [("c2", 1, 2), ("c2", 2, 6), ("c3", 1, 4), ("c4", 2, 4), ("c5", 1, 8)])
+def test_grid_shards_equal_single_plan_bitwise(name, B, world):
     cfg = SMALL[name]
     x, g = make_inputs(cfg)
-    B = min(cfg.batch, 2)
     x = x[:B].contiguous()
     pb, pk = grid_shape(B, cfg.K, world)
     assert pk > 1                                    # the K split is exercised
