@@ -425,7 +425,8 @@ def main():
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
-                                                                 "chunk_slabs", "gemm_variant", "in_slab_tiles")}}
+                                                                 "chunk_slabs", "gemm_variant", "in_slab_tiles",
+                                                                 "in_planes_per_cta")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
         if world == 1 and not args.no_cpu_baseline:

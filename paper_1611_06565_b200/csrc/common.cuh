@@ -12,6 +12,7 @@ namespace wino {
 
 constexpr int kMaxN = 4;      // spatial dims supported on the device path
 constexpr int kMaxA = 8;      // alpha <= 8 on the device path
+constexpr int kMaxPlanes = 8;  // input-transform slabs staged per CTA
 
 constexpr int ipow(int b, int e) { return e <= 0 ? 1 : b * ipow(b, e - 1); }
 
@@ -56,9 +57,11 @@ struct KGeom {
   int slab_bytes;            // bytes of the slab (one TMA box)
   int slot_bytes;            // slab slot stride (slab_bytes rounded up to 128)
   int hpitch;                // N = 3, alpha >= 6: row pitch of the axis-0 pass buffer H
-  int nslot;                 // slab slots: 2 = persistent CTAs prefetching the next plane
+  int hinplace;              // N = 3, alpha >= 6, bt0 = 1: the axis-0 pass overwrites the slab (no H)
+  int npl;                   // slabs per CTA (consecutive work items, one TMA box each)
+  int items_per_plane;       // transform work items of one slab
   int in_threads;            // block size of the input kernel (<= 256)
-  int smem_bytes;            // dynamic shared memory of the input kernel (nslot slabs + H)
+  int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

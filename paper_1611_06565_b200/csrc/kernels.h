@@ -11,6 +11,7 @@ enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
 
 bool xform_supported(int N, int alpha, int m, int spec);
 bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma);
+void plan_input_planes(KGeom& g, int64_t nwork, int num_sms);
 // a2: x [B][C][in...] -> V [P][C][T_s], input slabs [g.s_beg, g.s_beg + nslab)
 // (slab = b * nbox0 + box; V row = t - g.t0)
 // tm: TMA map of x from encode_input_map (NULL = cp.async fallback path)

@@ -325,6 +325,12 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   }
   p->device = device;
   DeviceGuard guard(device);
+  {
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) nsm = 148;
+    const int64_t nslab_all = p->chunked ? p->chunk_slabs : (int64_t)batch * g.nbox0;
+    plan_input_planes(g, nslab_all * C, nsm);
+  }
   const size_t ucount = (size_t)p->P * C * p->K_s;
   const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
   p->filter_bytes = ucount * 4 * nbuf;
@@ -557,9 +563,10 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
-  const int64_t v[18] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[19] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
-                         p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0};
+                         p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
+                         p->geom.npl};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

@@ -41,39 +41,57 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
     return (size_t)e0 * inner * 4;
   };
   auto hbytes = [&](int bt) { return hmode ? (size_t)bt * alpha * g.e[1] * g.hpitch * 4 : (size_t)0; };
-  // TMA path: two slab slots (persistent CTAs prefetch the next plane) if
-  // 2 slabs + H fit ~76 KB (3 CTAs / SM) for some bt0; else one slot, slab
-  // (+ H) near 64 KB (100 KB with H).
+  // one slab (+ H) near 64 KB (48 KB in H mode: measured c4 337 -> 288 us at bt0 = 1)
   int bt0 = g.tiles[0];
-  int nslot = 1;
-  // measured (c2, c4): the persistent prefetching variant is slower than
-  // one-shot CTAs; WINO_IN_SLOTS=2 enables it for experiments
-  const char* ev_slots = getenv("WINO_IN_SLOTS");
-  if (tma && N >= 2 && ev_slots && atoi(ev_slots) == 2) {
-    int bt = g.tiles[0];
-    while (bt > 1 && 2 * slab(bt) + hbytes(bt) > 76 * 1024) bt = (bt + 1) / 2;
-    if (2 * slab(bt) + hbytes(bt) <= 100 * 1024) {
-      nslot = 2;
-      bt0 = bt;
-    }
-  }
-  if (nslot == 1) {
-    size_t target = hmode ? 48 * 1024 : 64 * 1024;  // measured: c4 (H mode) 337 -> 288 us at bt0 = 1
-    if (const char* ev = getenv("WINO_IN_TARGET_KB")) target = (size_t)atoi(ev) * 1024;  // dev knob
-    while (bt0 > 1 && slab(bt0) + hbytes(bt0) > target) bt0 = (bt0 + 1) / 2;
-  }
-  if (nslot * (slab(bt0) + 128) + hbytes(bt0) > 200 * 1024) return false;
+  size_t target = hmode ? 48 * 1024 : 64 * 1024;
+  if (const char* ev = getenv("WINO_IN_TARGET_KB")) target = (size_t)atoi(ev) * 1024;  // dev knob
+  while (bt0 > 1 && slab(bt0) + hbytes(bt0) > target) bt0 = (bt0 + 1) / 2;
+  // H mode with a one-tile-deep slab: every slab column is private to the
+  // thread that transforms it along axis 0, so the pass writes its alpha
+  // outputs back into the column (no H buffer; several slabs fit a CTA)
+  const char* ev_inpl = getenv("WINO_IN_HINPLACE");  // dev knob: 0 keeps the separate H
+  g.hinplace = (hmode && bt0 == 1 && (!ev_inpl || atoi(ev_inpl) != 0)) ? 1 : 0;
+  const size_t hb = g.hinplace ? 0 : hbytes(bt0);
+  if (slab(bt0) + 128 + hb > 200 * 1024) return false;
   g.bt0 = bt0;
-  g.nslot = nslot;
+  g.npl = 1;  // plan_input_planes() raises it
   g.nbox0 = (g.tiles[0] + bt0 - 1) / bt0;
   g.e[0] = bt0 * m + halo;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
   g.in_threads = 256;
   if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256)
   g.slab_bytes = (int)slab(bt0);
+  g.items_per_plane = (N >= 3 ? alpha : 1) * bt0 * g.R;
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
-  g.smem_bytes = (int)(nslot * g.slot_bytes + hbytes(bt0));
+  g.smem_bytes = (int)(g.slot_bytes + hb);
   return true;
+}
+
+// Slabs per CTA (g.npl) for `nwork` work items: a CTA owns consecutive slabs
+// of one channel (one run of npl * bt0 * R tiles of t per (xi, c) in V) and
+// pools their work items.  Measured (B200): c2 (196 tile items per plane)
+// 37.3 -> 32.7 us at npl = 2, back to 37 at 3; c4 (294 items per plane) best
+// at 1 (0.29 -> 0.31 / 0.36 ms at 2 / 3): so about 1.6 blocks' worth of work
+// items per CTA, with slabs up to ~100 KB and >= 4 CTAs per SM of work.  Not
+// with a separate H buffer.
+void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
+  const bool pooled = g.hinplace || g.hpitch == 0;
+  int npl = 1;
+  if (pooled) {
+    // work items per plane: tiles (N <= 2) or (xi_0, tile) pairs (N >= 3)
+    const int items = g.items_per_plane;
+    npl = (int)((1.6 * g.in_threads) / (items > 0 ? items : 1));
+    const int by_smem = (int)((100 * 1024) / g.slot_bytes);
+    if (npl > by_smem) npl = by_smem;
+    const int64_t cap = nwork / (4LL * num_sms);
+    if (npl > cap) npl = (int)cap;
+  }
+  if (const char* ev = getenv("WINO_IN_NPL")) npl = atoi(ev);  // dev knob
+  if (npl < 1) npl = 1;
+  if (npl > kMaxPlanes) npl = kMaxPlanes;
+  if (!pooled) npl = 1;
+  g.npl = npl;
+  g.smem_bytes = npl * g.slot_bytes + (pooled ? 0 : (g.smem_bytes - g.slot_bytes));
 }
 
 // TMA descriptor of x viewed as (in_{N-1}, .., in_0, B*C) with the slab box;

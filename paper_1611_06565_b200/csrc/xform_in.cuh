@@ -209,47 +209,110 @@ __device__ __forceinline__ void issue_slab_tma(float* S, const CUtensorMap* tm, 
   tma_load_slab((uint32_t)__cvta_generic_to_shared(S), tm, co, bar, N + 1);
 }
 
-// Transform one staged plane: slab S -> V rows of tiles [a0, a0 + nt0) x (all).
+// One staged plane of a CTA's group (the CTA owns npl consecutive work items
+// w0 .. w0+npl-1: consecutive slabs of one channel, i.e. one contiguous run
+// of t per (xi, c) in V).
+struct PlaneInfo {
+  int b, a0, nt0, c;
+};
+
+// Transform the CTA's npl staged planes: slab p at S0 + p * slab_f -> V rows
+// of its tiles.  Work items of all planes form one pool, so every round of
+// the block keeps all warps busy and the V stores of neighbouring planes
+// (adjacent t) are issued together.
 template <int N, int A, int M, class Tab, int D>
-__device__ __forceinline__ void transform_plane(const float* __restrict__ S, float* __restrict__ H, float* __restrict__ V,
-                                                const KGeom& g, const XfParams& xp, int b, int a0, int nt0, int c) {
+__device__ __forceinline__ void transform_planes(float* __restrict__ S0, int slab_f, float* __restrict__ H,
+                                                 float* __restrict__ V, const KGeom& g, const XfParams& xp,
+                                                 const PlaneInfo* pl, int npl) {
+  const int64_t pstride = (int64_t)g.C * g.T_s;
+  auto vbase = [&](int p) -> float* {
+    return V + (int64_t)pl[p].c * g.T_s + ((int64_t)pl[p].b * g.Tps + (int64_t)pl[p].a0 * g.R - g.t0);
+  };
   // ---- N = 3, alpha >= 6: the axis-0 pass materialised in shared memory
   if constexpr (N == 3 && A >= 6) {
     using Get = BTget<Tab>;
-    const int e1 = g.e[1], e2 = g.e[2], hp = g.hpitch;
-    // H: [t0][xi_0][y][x], window rows 16-byte aligned
-    // phase 1: one thread per (t0, y, x) column: alpha values along axis 0
-    // (conflict-free scalar LDS, lanes = consecutive x) -> alpha xi_0 outputs
-    for (int w = threadIdx.x; w < nt0 * e1 * hp; w += blockDim.x) {
-      const int xh = w % hp, r = w / hp;
-      if (xh >= e2) continue;
-      const int y = r % e1, t0l = r / e1;
-      const float* col = S + t0l * M * g.sst[0] + y * g.sst[1] + xh + D;
-      float v[A];
+    const int e1 = g.e[1], e2 = g.e[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int tl1 = g.tiles[1], tl2 = g.tiles[2];
+    if (g.hinplace) {
+      // bt0 = 1: phase 1 rewrites every slab column (y, x) in place with its
+      // alpha axis-0 outputs (the column is private to its thread; lanes =
+      // consecutive x, conflict-free)
+      for (int r = warp; r < npl * e1; r += nwarps) {
+        const int p = r / e1, y = r - p * e1;
+        float* row = S0 + p * slab_f + y * g.sst[1] + D;
+        for (int xh = lane; xh < e2; xh += 32) {
+          float* col = row + xh;
+          float v[A];
 #pragma unroll
-      for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
-      float* hrow = H + (t0l * A * e1 + y) * hp + xh;
+          for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
 #pragma unroll
-      for (int x0 = 0; x0 < A; ++x0) {
-        float acc = 0.f;
-        bool first = true;
+          for (int x0 = 0; x0 < A; ++x0) {
+            float acc = 0.f;
+            bool first = true;
 #pragma unroll
-        for (int i = 0; i < A; ++i) {
-          if (Get::nz(xp, x0, i)) {
-            acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
-            first = false;
+            for (int i = 0; i < A; ++i) {
+              if (Get::nz(xp, x0, i)) {
+                acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
+                first = false;
+              }
+            }
+            col[x0 * g.sst[0]] = acc;
           }
         }
-        hrow[x0 * e1 * hp] = acc;
+      }
+      __syncthreads();
+      // phase 2: one work item per (plane, xi_0, t1, t2) on plane xi_0 of its slab
+      const int R = tl1 * tl2, nper = A * R;
+      for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
+        const int p = u / nper;
+        const int w = u - p * nper;
+        const int xi0 = w / R;
+        const int tl = w - xi0 * R;
+        const int t1 = tl / tl2, t2 = tl - t1 * tl2;
+        const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
+        float h[A * A];
+#pragma unroll
+        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, D>(hp0 + i1 * g.sst[1], h + i1 * A);
+        all_axes<A, 2, A, A, Get>(h, xp);
+        float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
+#pragma unroll
+        for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
+      }
+      return;
+    }
+    // separate H buffer (npl = 1): H = [t0][xi_0][y][x], window rows 16-byte aligned
+    const PlaneInfo& q = pl[0];
+    const int hp = g.hpitch, nt0 = q.nt0;
+    // phase 1: one thread per (t0, y, x) column: alpha values along axis 0
+    // (conflict-free scalar LDS, lanes = consecutive x) -> alpha xi_0 outputs
+    for (int r = warp; r < nt0 * e1; r += nwarps) {
+      const int y = r % e1, t0l = r / e1;
+      for (int xh = lane; xh < e2; xh += 32) {
+        const float* col = S0 + t0l * M * g.sst[0] + y * g.sst[1] + xh + D;
+        float v[A];
+#pragma unroll
+        for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
+        float* hrow = H + (t0l * A * e1 + y) * hp + xh;
+#pragma unroll
+        for (int x0 = 0; x0 < A; ++x0) {
+          float acc = 0.f;
+          bool first = true;
+#pragma unroll
+          for (int i = 0; i < A; ++i) {
+            if (Get::nz(xp, x0, i)) {
+              acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
+              first = false;
+            }
+          }
+          hrow[x0 * e1 * hp] = acc;
+        }
       }
     }
     __syncthreads();
     // phase 2: one work item per (t0, xi_0, t1, t2): the alpha x alpha window
     // of plane (t0, xi_0) in registers, axes 1 and 2 transformed in place
-    const int tl1 = g.tiles[1], tl2 = g.tiles[2];
-    const int64_t pstride = (int64_t)g.C * g.T_s;
-    const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;
-    float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
+    float* __restrict__ vb = vbase(0);
     for (int w = threadIdx.x; w < nt0 * A * tl1 * tl2; w += blockDim.x) {
       const int t2 = w % tl2;
       int r = w / tl2;
@@ -261,22 +324,40 @@ __device__ __forceinline__ void transform_plane(const float* __restrict__ S, flo
 #pragma unroll
       for (int i1 = 0; i1 < A; ++i1) load_row<A, M, 0>(hp0 + i1 * hp, h + i1 * A);
       all_axes<A, 2, A, A, Get>(h, xp);
-      float* vo = vbase + (t0l * tl1 + t1) * tl2 + t2 + (int64_t)xi0 * (A * A) * pstride;
+      float* vo = vb + (t0l * tl1 + t1) * tl2 + t2 + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
       for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
     }
-    return;
   } else {
-
-  // ---- 2./3. work items (xi_0, tile), tile fastest
-    const int ntile = nt0 * g.R;
-    constexpr int NX = N >= 3 ? A : 1;  // work items per tile (one per xi_0 when N >= 3)
-    const int64_t pstride = (int64_t)g.C * g.T_s;
-    const int64_t t0g = (int64_t)b * g.Tps + (int64_t)a0 * g.R - g.t0;  // V row of the slab's first tile
-    float* __restrict__ vbase = V + (int64_t)c * g.T_s + t0g;
-    for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
+    // ---- work items (plane, xi_0, tile), tile fastest
+    constexpr int NX = N >= 3 ? A : 1;        // work items per tile (one per xi_0 when N >= 3)
+    if (npl == 1) {
+      // one plane: no plane index to decode (the common case for large slabs)
+      const int ntile = pl[0].nt0 * g.R;
+      float* __restrict__ vb = vbase(0);
+      for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
+        const int xi0 = w / ntile;
+        const int tl = w - xi0 * ntile;
+        int rem = tl, base = 0;
+#pragma unroll
+        for (int ax = N - 1; ax >= 1; --ax) {
+          const int ti = rem % g.tiles[ax];
+          rem /= g.tiles[ax];
+          base += ti * M * g.sst[ax];
+        }
+        base += rem * M * g.sst[0];
+        in_dispatch<N, A, M, Tab, D>(xi0, S0, base, g, xp, vb + tl, pstride);
+      }
+      return;
+    }
+    const int ntile = g.bt0 * g.R;            // tiles of a full-depth slab
+    const int nper = NX * ntile;
+    for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
+      const int p = u / nper;
+      const int w = u - p * nper;
       const int xi0 = w / ntile;
       const int tl = w - xi0 * ntile;
+      if (tl >= pl[p].nt0 * g.R) continue;    // last axis-0 box of a sample is shorter
       // local tile -> slab offset of its window
       int rem = tl, base = 0;
 #pragma unroll
@@ -286,115 +367,78 @@ __device__ __forceinline__ void transform_plane(const float* __restrict__ S, flo
         base += ti * M * g.sst[ax];
       }
       base += rem * M * g.sst[0];
-      in_dispatch<N, A, M, Tab, D>(xi0, S, base, g, xp, vbase + tl, pstride);
+      in_dispatch<N, A, M, Tab, D>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride);
     }
   }
 }
 
-// One work item = one (b, c) plane slab (tiles [a0, a0 + bt0) of axis 0).
-// Persistent: CTA i handles planes i, i + G, ...; with kTma the slab of the
-// next plane is prefetched into the second slot while the current one is
-// transformed (g.nslot = 2), hiding the TMA latency behind the compute.
-// kTma (N >= 2): slab via one TMA box starting D columns left of -P_last.
-// !kTma: cp.async fallback, D == 0, one slot.
+// A CTA owns npl = g.npl consecutive work items w (one (b, c) plane slab =
+// tiles [a0, a0 + bt0) of axis 0 each; consecutive w are consecutive slabs of
+// the same channel).  kTma (N >= 2): each slab is one TMA box starting D
+// columns left of -P_last, all npl boxes issued at once; !kTma: cp.async
+// fallback, D == 0.
 template <int N, int A, int M, class Tab, int D, bool kTma>
 __global__ void __launch_bounds__(256)
 k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
               const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm, int nslab) {
   extern __shared__ __align__(128) float smem_f[];
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[kMaxPlanes];
+  __shared__ PlaneInfo pl[kMaxPlanes];
   const int slab_f = g.slot_bytes / 4;  // slot stride: 128-byte aligned TMA destinations
-  float* H = smem_f + g.nslot * slab_f;
+  float* H = smem_f + g.npl * slab_f;
   const int nwork = nslab * g.C;
-  auto plane = [&](int w, int& b, int& a0, int& nt0, int& c) {
+  const int w0 = blockIdx.x * g.npl;
+  const int npl = min(g.npl, nwork - w0);
+  auto plane = [&](int w) {
+    PlaneInfo q;
     const int64_t slab = g.s_beg + w % nslab;
-    c = w / nslab;
-    b = (int)(slab / g.nbox0);
-    const int box = (int)(slab - (int64_t)b * g.nbox0);
-    a0 = box * g.bt0;
-    nt0 = min(g.bt0, g.tiles[0] - a0);
+    q.c = w / nslab;
+    q.b = (int)(slab / g.nbox0);
+    const int box = (int)(slab - (int64_t)q.b * g.nbox0);
+    q.a0 = box * g.bt0;
+    q.nt0 = min(g.bt0, g.tiles[0] - q.a0);
+    return q;
   };
+  if (threadIdx.x < npl) pl[threadIdx.x] = plane(w0 + threadIdx.x);
   pdl_wait();      // x may come from the preceding kernel; V is read by the previous GEMM
   pdl_trigger();
   if constexpr (kTma) {
     static_assert(N >= 2, "TMA slab path needs N >= 2");
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
     if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8) : "memory");
+      for (int p = 0; p < npl; ++p) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u * p) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      if ((int)blockIdx.x < nwork) {
-        int b, a0, nt0, c;
-        plane(blockIdx.x, b, a0, nt0, c);
-        issue_slab_tma<N, M, D>(smem_f, &tm, g, b, a0, c, mb0);
+      for (int p = 0; p < npl; ++p) {
+        const PlaneInfo q = plane(w0 + p);
+        issue_slab_tma<N, M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, mb0 + 8u * p);
       }
     }
     __syncthreads();
-    uint32_t ph = 0;  // bit s: phase of slot s
-    int it = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++it) {
-      const int cur = g.nslot == 2 ? (it & 1) : 0;
-      const int wn = w + gridDim.x;
-      if (g.nslot == 2 && threadIdx.x == 0 && wn < nwork) {
-        // the other slot's last reader finished before the previous iteration's trailing barrier
-        int b, a0, nt0, c;
-        plane(wn, b, a0, nt0, c);
-        issue_slab_tma<N, M, D>(smem_f + (cur ^ 1) * slab_f, &tm, g, b, a0, c, mb0 + 8u * (cur ^ 1));
-      }
-      const uint32_t mbc = mb0 + 8u * cur;
+    for (int p = 0; p < npl; ++p) {
       uint32_t done = 0;
       while (!done) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(mbc), "r"((ph >> cur) & 1u)
+            : "r"(mb0 + 8u * p)
             : "memory");
-      }
-      ph ^= 1u << cur;
-      int b, a0, nt0, c;
-      plane(w, b, a0, nt0, c);
-      transform_plane<N, A, M, Tab, D>(smem_f + cur * slab_f, H, V, g, xp, b, a0, nt0, c);
-      __syncthreads();
-      if (g.nslot == 1 && threadIdx.x == 0 && wn < nwork) {
-        int b2, a2, nt2, c2;
-        plane(wn, b2, a2, nt2, c2);
-        issue_slab_tma<N, M, D>(smem_f, &tm, g, b2, a2, c2, mb0);
       }
     }
   } else {
     static_assert(D == 0, "the cp.async slab path is unshifted");
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-      int b, a0, nt0, c;
-      plane(w, b, a0, nt0, c);
-      load_slab_cpasync<N, A, M>(smem_f, x, g, b, a0, nt0, c);
-      __syncthreads();
-      transform_plane<N, A, M, Tab, 0>(smem_f, H, V, g, xp, b, a0, nt0, c);
-      __syncthreads();
-    }
+    __syncthreads();
+    for (int p = 0; p < npl; ++p)
+      load_slab_cpasync<N, A, M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c);
+    __syncthreads();
   }
+  transform_planes<N, A, M, Tab, D>(smem_f, slab_f, H, V, g, xp, pl, npl);
 }
 
 template <class K>
 inline cudaError_t set_smem(K kern, int bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  // the opt-in limit covers dynamic + static shared memory (barriers, plane table)
+  if (bytes <= 46 * 1024) return cudaSuccess;
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
-
-// Launch one (N, alpha, m, table) instantiation.  tm != NULL selects the TMA
-// slab (g.dL is its column shift, 0 or 3); kAllowTma = false compiles only the
-// fallback (run-time tables).
-// Slabs [g.s_beg, g.s_beg + nslab) of the flattened (b, box) order.
-// CTAs per SM of one instantiation at `smem` bytes (cached per instantiation).
-template <class K>
-inline int occupancy(K kern, int smem, int threads) {
-  static int cached_smem = -1, cached = 1;
-  if (cached_smem != smem) {
-    int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess || n < 1) n = 1;
-    cached = n;
-    cached_smem = smem;
-  }
-  return cached;
 }
 
 template <class K>
@@ -403,13 +447,7 @@ inline cudaError_t launch_in_kern(K kern, const float* x, float* V, const KGeom&
   cudaError_t e;
   if ((e = set_smem(kern, g.smem_bytes)) != cudaSuccess) return e;
   const long long nwork = (long long)nslab * g.C;
-  long long grid = nwork;
-  if (g.nslot == 2) {  // persistent: enough CTAs to fill the SMs, each prefetching its next plane
-    static int sms = 0;
-    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
-    const long long cap = (long long)occupancy(kern, g.smem_bytes, g.in_threads) * sms;
-    if (grid > cap) grid = cap;
-  }
+  const long long grid = (nwork + g.npl - 1) / g.npl;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(g.in_threads), g.smem_bytes, s, x, V, g, xp, tm, nslab);
 }
 
@@ -424,7 +462,6 @@ cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& 
     if (tm && g.dL == 3) return launch_in_kern(k_input_xform<N, A, M, Tab, 3, true>, x, V, g, xp, *tm, nslab, s);
   }
   KGeom g1 = g;
-  g1.nslot = 1;
   CUtensorMap dummy{};
   return launch_in_kern(k_input_xform<N, A, M, Tab, 0, false>, x, V, g1, xp, dummy, nslab, s);
 }
