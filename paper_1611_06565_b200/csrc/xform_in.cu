@@ -61,31 +61,22 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
   g.in_threads = 256;
   if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256)
   g.slab_bytes = (int)slab(bt0);
-  g.items_per_plane = (N >= 3 ? alpha : 1) * bt0 * g.R;
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(g.slot_bytes + hb);
   return true;
 }
 
 // Slabs per CTA (g.npl) for `nwork` work items: a CTA owns consecutive slabs
-// of one channel (one run of npl * bt0 * R tiles of t per (xi, c) in V) and
-// pools their work items.  Measured (B200): c2 (196 tile items per plane)
-// 37.3 -> 32.7 us at npl = 2, back to 37 at 3; c4 (294 items per plane) best
-// at 1 (0.29 -> 0.31 / 0.36 ms at 2 / 3): so about 1.6 blocks' worth of work
-// items per CTA, with slabs up to ~100 KB and >= 4 CTAs per SM of work.  Not
-// with a separate H buffer.
+// of one channel (adjacent runs of t in V) and pools their work items, xi_0
+// outermost in H mode, so each round of the block stores long runs of t per
+// plane of V.  Measured (B200, tools/in_sweep.sh): c2 37.1 -> 32.8 us and c4
+// 0.297 -> 0.247 ms at npl = 2, both worse at 3 and 4 -> two slabs per CTA
+// when they fit 64 KB, keeping >= 4 CTAs per SM of work.  Not with a
+// separate H buffer.
 void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
   const bool pooled = g.hinplace || g.hpitch == 0;
   int npl = 1;
-  if (pooled) {
-    // work items per plane: tiles (N <= 2) or (xi_0, tile) pairs (N >= 3)
-    const int items = g.items_per_plane;
-    npl = (int)((1.6 * g.in_threads) / (items > 0 ? items : 1));
-    const int by_smem = (int)((100 * 1024) / g.slot_bytes);
-    if (npl > by_smem) npl = by_smem;
-    const int64_t cap = nwork / (4LL * num_sms);
-    if (npl > cap) npl = (int)cap;
-  }
+  if (pooled && 2 * g.slot_bytes <= 64 * 1024 && nwork / 2 >= 4LL * num_sms) npl = 2;
   if (const char* ev = getenv("WINO_IN_NPL")) npl = atoi(ev);  // dev knob
   if (npl < 1) npl = 1;
   if (npl > kMaxPlanes) npl = kMaxPlanes;

@@ -262,13 +262,16 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         }
       }
       __syncthreads();
-      // phase 2: one work item per (plane, xi_0, t1, t2) on plane xi_0 of its slab
-      const int R = tl1 * tl2, nper = A * R;
-      for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
-        const int p = u / nper;
-        const int w = u - p * nper;
-        const int xi0 = w / R;
-        const int tl = w - xi0 * R;
+      // phase 2: one work item per (xi_0, plane, t1, t2) on plane xi_0 of its
+      // slab; xi_0 outermost, so a round of the block writes long runs of t
+      // (npl planes are adjacent in t) into each of the alpha^2 planes of V
+      // it touches (measured: the V store pattern bounds this kernel)
+      const int R = tl1 * tl2, nrun = npl * R;
+      for (int u = threadIdx.x; u < A * nrun; u += blockDim.x) {
+        const int xi0 = u / nrun;
+        const int w = u - xi0 * nrun;
+        const int p = w / R;
+        const int tl = w - p * R;
         const int t1 = tl / tl2, t2 = tl - t1 * tl2;
         const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
         float h[A * A];

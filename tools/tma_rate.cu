@@ -22,6 +22,8 @@ __device__ __forceinline__ void wait_bar(uint32_t mb, uint32_t ph) {
 
 __global__ void k(const __grid_constant__ CUtensorMap tm, const float* x, int P, int mode, int slots, int slot_bytes,
                   int bytes, unsigned long long* sink) {
+  // modes 5/6 (c4 geometry): plane p = (b*C + c) * 2 + depth box
+
   extern __shared__ __align__(128) unsigned char S[];
   __shared__ __align__(8) uint64_t bar[8];
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
@@ -45,6 +47,14 @@ __global__ void k(const __grid_constant__ CUtensorMap tm, const float* x, int P,
     } else if (mode == 1) {
       asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                    ::"r"(dst), "l"(&tm), "r"(0), "r"(p * 14), "r"(mb) : "memory");
+    } else if (mode == 5) {
+      const int bc = p >> 1, d0 = (p & 1) * 4 - 1;
+      asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                   ::"r"(dst), "l"(&tm), "r"(-4), "r"(-1), "r"(d0), "r"(bc), "r"(mb) : "memory");
+    } else if (mode == 6) {
+      const int bc = p >> 1, d0 = (p & 1) * 4;  // 4..6 planes in range: copy 4 planes + 1 halo (5 x 3136 B)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(x + (size_t)bc * 6272 + (size_t)(d0 > 0 ? d0 - 1 : 0) * 784), "r"(5 * 3136), "r"(mb) : "memory");
     } else if (mode == 2) {
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                    ::"r"(dst), "l"(x + (size_t)p * 3136), "r"(12544), "r"(mb) : "memory");
@@ -84,10 +94,26 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   int nsm = 148;
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     CUtensorMap tm{};
     int bytes;
-    if (mode == 0 || mode == 3) {
+    int Pm = P;
+    double payload = 12544;
+    if (mode == 4) continue;
+    if (mode == 5 || mode == 6) {
+      // x viewed as [BC][8][28][28] (c4 planes), 2 depth boxes per (b, c)
+      const cuuint64_t BC = (cuuint64_t)P * 3136 / 6272;
+      Pm = (int)(BC * 2);
+      cuuint64_t dims[4] = {28, 28, 8, BC};
+      cuuint64_t strides[3] = {28 * 4, 784 * 4, 6272 * 4};
+      cuuint32_t box[4] = {36, 30, 6, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r) { printf("enc %d\n", r); return 1; }
+      bytes = mode == 5 ? 36 * 30 * 6 * 4 : 5 * 3136;
+      payload = 3136.0 * 4;  // unique x bytes per box (4 of 8 depth planes)
+    } else if (mode == 0 || mode == 3) {
       cuuint64_t dims[3] = {56, 56, (cuuint64_t)P};
       cuuint64_t strides[2] = {56 * 4, 56 * 56 * 4};
       cuuint32_t box[3] = {mode == 0 ? 64u : 56u, mode == 0 ? 58u : 56u, 1};
@@ -113,17 +139,17 @@ int main(int argc, char** argv) {
         if (smem * cps > 220 * 1024) continue;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int grid = nsm * cps;
-        for (int w = 0; w < 2; ++w) k<<<grid, 32, smem>>>(tm, x, P, mode, slots, slot_bytes, bytes, sink);
+        for (int w = 0; w < 2; ++w) k<<<grid, 32, smem>>>(tm, x, Pm, mode, slots, slot_bytes, bytes, sink);
         cudaEventRecord(e0);
         const int reps = 5;
-        for (int rr = 0; rr < reps; ++rr) k<<<grid, 32, smem>>>(tm, x, P, mode, slots, slot_bytes, bytes, sink);
+        for (int rr = 0; rr < reps; ++rr) k<<<grid, 32, smem>>>(tm, x, Pm, mode, slots, slot_bytes, bytes, sink);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         cudaError_t err = cudaGetLastError();
-        const double gbs = (double)P * 12544 * reps / (ms * 1e-3) / 1e9;
-        printf("mode %d cta/sm %d slots %d  %.1f us/launch  %.0f GB/s (payload 12544 B/plane) %s\n", mode, cps, slots,
+        const double gbs = (double)Pm * payload * reps / (ms * 1e-3) / 1e9;
+        printf("mode %d cta/sm %d slots %d  %.1f us/launch  %.0f GB/s (unique x) %s\n", mode, cps, slots,
                ms * 1e3 / reps, gbs, err ? cudaGetErrorString(err) : "");
       }
     }
