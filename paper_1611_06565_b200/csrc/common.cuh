@@ -13,6 +13,7 @@ namespace wino {
 constexpr int kMaxN = 4;      // spatial dims supported on the device path
 constexpr int kMaxA = 8;      // alpha <= 8 on the device path
 constexpr int kMaxPlanes = 8;  // input-transform slabs staged per CTA
+constexpr int kMaxOutStages = 8;  // output-transform TMA ring depth
 
 constexpr int ipow(int b, int e) { return e <= 0 ? 1 : b * ipow(b, e - 1); }
 

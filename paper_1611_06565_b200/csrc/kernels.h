@@ -19,8 +19,10 @@ bool encode_input_map(CUtensorMap* tm, const float* x, const KGeom& g, int N, in
 cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
                                const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
 // a4: M [P][K][T_s] -> y [B][K][out...] for tiles [g.t_beg, g.T) (M row = t - g.t0)
+// tmM: TMA map of M from encode_output_map (NULL = plain per-thread loads)
+bool encode_output_map(CUtensorMap* tm, const float* Mx, int64_t T_s, int K, int64_t P, int A1);
 cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
-                                const XfParams& xp, cudaStream_t s);
+                                const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s);
 

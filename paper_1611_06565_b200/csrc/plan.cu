@@ -188,6 +188,8 @@ struct wino_plan_s {
   bool filter_ready = false;
   TcGemm tg{};
   CUtensorMap tm_x{};          // input-transform TMA map (cached per x pointer / B)
+  CUtensorMap tm_M{};          // output-transform TMA map of M (fixed workspace)
+  bool tm_M_ok = false;
   const float* tm_x_ptr = nullptr;
   int tm_x_B = 0;
   bool tm_x_ok = false;
@@ -353,6 +355,13 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
     delete p;
     return fail(WINO_ERR_CUDA, "workspace memset failed: %s", cudaGetErrorString(e));
   }
+  {
+    // a4 reads M through TMA boxes unless disabled (WINO_OUT_TMA=0, dev knob)
+    const char* ev = getenv("WINO_OUT_TMA");
+    int64_t A1 = 1;
+    for (int n = 1; n < N; ++n) A1 *= a;
+    p->tm_M_ok = (!ev || atoi(ev) != 0) && encode_output_map(&p->tm_M, p->M, p->T_s, K, p->P, (int)A1);
+  }
   if (p->gemm_mode == WINO_GEMM_FFMA) {
     p->U32 = p->ubuf;
   } else {
@@ -473,7 +482,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(pg.end());
     ProfScope po{p, s, 2};
     if (rec) CUDA_TRY(po.begin());
-    CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, s));
+    CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, p->tm_M_ok ? &p->tm_M : nullptr, s));
     if (rec) CUDA_TRY(po.end());
   }
   if (rec) ++p->prof_calls;

@@ -2,6 +2,7 @@
 // transform:  U_xi[c][k] = (g[k, c] x_1 G ... x_N G)_xi  (Eq. (4),
 // PAPER.md:160-164; cached transformed kernels PAPER.md:178).
 #include "kernels.h"
+#include "tma.hpp"
 #include "xform_out.cuh"
 
 namespace wino {
@@ -59,9 +60,23 @@ bool xform_supported(int N, int alpha, int m, int spec) {
 }
 
 cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
-                                const XfParams& xp, cudaStream_t s) {
-  if (spec != kSpecRuntime) return launch_output_const(N, alpha, m, spec, Mx, y, g, xp, s);
-  return launch_output_run(N, alpha, m, Mx, y, g, xp, s);
+                                const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s) {
+  if (spec != kSpecRuntime) return launch_output_const(N, alpha, m, spec, Mx, y, g, xp, tmM, s);
+  return launch_output_run(N, alpha, m, Mx, y, g, xp, tmM, s);
+}
+
+// TMA map of M [P][K][T_s] as (t, k, xi) with the output kernel's box
+// {128, 1, alpha^(N-1)}; false if a TMA rule is broken (plain kernel then).
+bool encode_output_map(CUtensorMap* tm, const float* Mx, int64_t T_s, int K, int64_t P, int A1) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc || A1 > 256 || ((uintptr_t)Mx & 15) || (T_s % 128)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)T_s, (cuuint64_t)K, (cuuint64_t)P};
+  cuuint64_t strides[2] = {(cuuint64_t)T_s * 4, (cuuint64_t)T_s * K * 4};
+  cuuint32_t box[3] = {128, 1, (cuuint32_t)A1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(Mx), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,

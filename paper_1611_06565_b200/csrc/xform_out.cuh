@@ -14,43 +14,30 @@ namespace out_detail {
 // ------------------------------------------------------------------ a4
 // One thread per (tile t, output channel k): read M[xi][k][t] for all xi,
 // apply A^T along every axis (alpha -> m), crop to `out` and scatter into y.
+
+// Accumulate axis-0 group x1 (the alpha^(N-1) values v of M[xi][k][t] with
+// xi_0 = x1) into the output tile o: A^T along axes 1..N-1 in registers,
+// then o += A^T[:, x1] (x) v along axis 0.
 template <int N, int A, int M, class Tab>
-__global__ void __launch_bounds__(128)
-k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid_constant__ KGeom g,
-               const __grid_constant__ XfParams xp) {
-  constexpr int A1 = ipow(A, N - 1);
+__device__ __forceinline__ void accum_group(float (&o)[ipow(M, N)], float (&v)[ipow(A, N - 1)], int x1,
+                                            const XfParams& xp) {
+  constexpr int M1 = ipow(M, N - 1);
+  all_axes<A, N - 1, M, M, ATget<Tab>>(v, xp);
+#pragma unroll
+  for (int o1 = 0; o1 < M; ++o1) {
+    if (!ATget<Tab>::nz(xp, o1, x1)) continue;
+    const float av = ATget<Tab>::v(xp, o1, x1);
+#pragma unroll
+    for (int rr = 0; rr < M1; ++rr)
+      o[o1 * M1 + rr] = fmaf(av, v[digits_to_base(rr, N - 1, M, A)], o[o1 * M1 + rr]);
+  }
+}
+
+template <int N, int M>
+__device__ __forceinline__ void store_tile(float (&o)[ipow(M, N)], float* __restrict__ y, const KGeom& g, int64_t t,
+                                           int k) {
   constexpr int M1 = ipow(M, N - 1);
   constexpr int MN = ipow(M, N);
-  pdl_wait();      // M comes from the GEMM
-  pdl_trigger();
-  const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
-  const int k = blockIdx.y;
-  if (t >= g.T) return;
-  const int64_t pstride = (int64_t)g.K * g.T_s;
-  // running pointer over the alpha^N points (one 64-bit add per load instead
-  // of a 64-bit multiply-add per point offset)
-  const float* src = Mx + (int64_t)k * g.T_s + (t - g.t0);
-  float o[MN];
-#pragma unroll
-  for (int j = 0; j < MN; ++j) o[j] = 0.f;
-#pragma unroll
-  for (int x1 = 0; x1 < A; ++x1) {
-    float v[A1];
-#pragma unroll
-    for (int j = 0; j < A1; ++j) {
-      v[j] = __ldg(src);
-      src += pstride;
-    }
-    all_axes<A, N - 1, M, M, ATget<Tab>>(v, xp);
-#pragma unroll
-    for (int o1 = 0; o1 < M; ++o1) {
-      if (!ATget<Tab>::nz(xp, o1, x1)) continue;
-      const float av = ATget<Tab>::v(xp, o1, x1);
-#pragma unroll
-      for (int rr = 0; rr < M1; ++rr)
-        o[o1 * M1 + rr] = fmaf(av, v[digits_to_base(rr, N - 1, M, A)], o[o1 * M1 + rr]);
-    }
-  }
   // Eq. (2) epilogue in the spatial domain: d' = f(b + conv)
   if (g.bias || g.act) {
     const float bk = g.bias ? __ldg(g.bias + k) : 0.f;
@@ -104,19 +91,161 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
 }
 
 template <int N, int A, int M, class Tab>
-cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams& xp, cudaStream_t s) {
+__global__ void __launch_bounds__(128)
+k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid_constant__ KGeom g,
+               const __grid_constant__ XfParams xp) {
+  constexpr int A1 = ipow(A, N - 1);
+  constexpr int MN = ipow(M, N);
+  pdl_wait();      // M comes from the GEMM
+  pdl_trigger();
+  const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const int k = blockIdx.y;
+  if (t >= g.T) return;
+  const int64_t pstride = (int64_t)g.K * g.T_s;
+  // running pointer over the alpha^N points (one 64-bit add per load instead
+  // of a 64-bit multiply-add per point offset)
+  const float* src = Mx + (int64_t)k * g.T_s + (t - g.t0);
+  float o[MN];
+#pragma unroll
+  for (int j = 0; j < MN; ++j) o[j] = 0.f;
+#pragma unroll
+  for (int x1 = 0; x1 < A; ++x1) {
+    float v[A1];
+#pragma unroll
+    for (int j = 0; j < A1; ++j) {
+      v[j] = __ldg(src);
+      src += pstride;
+    }
+    accum_group<N, A, M, Tab>(o, v, x1, xp);
+  }
+  store_tile<N, M>(o, y, g, t, k);
+}
+
+// TMA-fed variant (persistent): a CTA of 128 threads walks units (t-block of
+// 128 tiles, k), consecutive units = adjacent t-blocks of one k.  Each unit
+// is alpha groups (one per xi_0) of alpha^(N-1) x 128 floats of M, loaded by
+// one TMA box {128 t, 1 k, alpha^(N-1) xi} into a ring of `ns` stages that
+// runs ns - 1 groups ahead (across unit boundaries); threads read their
+// column (conflict-free) and accumulate as above.  Keeps tens of KB of M in
+// flight per SM without the per-thread load latency of the plain kernel.
+template <int N, int A, int M, class Tab>
+__global__ void __launch_bounds__(128)
+k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const __grid_constant__ XfParams xp,
+                   const __grid_constant__ CUtensorMap tmM, int ns) {
+  constexpr int A1 = ipow(A, N - 1);
+  constexpr int MN = ipow(M, N);
+  constexpr uint32_t kStageBytes = A1 * 128 * 4;
+  extern __shared__ __align__(128) float S[];
+  __shared__ __align__(8) uint64_t full[kMaxOutStages];
+  const int nblk = (int)((g.T - g.t_beg + 127) / 128);
+  const int64_t nunits = (int64_t)nblk * g.K;
+  const uint32_t fb0 = (uint32_t)__cvta_generic_to_shared(&full[0]);
+  const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(S);
+  // group q of this CTA: its (q / A)-th unit, xi_0 = q % A
+  auto issue = [&](int64_t q, int st) {
+    const int64_t u = blockIdx.x + (q / A) * gridDim.x;
+    if (u >= nunits) return;
+    const int k = (int)(u / nblk), tb = (int)(u - (int64_t)k * nblk);
+    const int tc = (int)(g.t_beg - g.t0) + tb * 128;
+    const uint32_t bar = fb0 + 8u * st;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStageBytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(sb0 + st * kStageBytes), "l"(&tmM), "r"(tc), "r"(k), "r"((int)(q % A) * A1), "r"(bar)
+        : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < ns; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fb0 + 8u * st) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();      // M comes from the GEMM
+  pdl_trigger();
+  if (threadIdx.x == 0)
+    for (int st = 0; st < ns; ++st) issue(st, st);
+  int64_t q = 0;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int k = (int)(u / nblk), tb = (int)(u - (int64_t)k * nblk);
+    const int64_t t = g.t_beg + (int64_t)tb * 128 + threadIdx.x;
+    float o[MN];
+#pragma unroll
+    for (int j = 0; j < MN; ++j) o[j] = 0.f;
+#pragma unroll
+    for (int x1 = 0; x1 < A; ++x1, ++q) {
+      const int st = (int)(q % ns);
+      const uint32_t par = (uint32_t)((q / ns) & 1);
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(fb0 + 8u * st), "r"(par)
+            : "memory");
+      }
+      float v[A1];
+      const float* col = S + st * (A1 * 128) + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < A1; ++j) v[j] = col[j * 128];
+      __syncthreads();  // every thread has read stage st: refill it ns groups ahead
+      if (threadIdx.x == 0) issue(q + ns, st);
+      accum_group<N, A, M, Tab>(o, v, x1, xp);
+    }
+    if (t < g.T) store_tile<N, M>(o, y, g, t, k);
+  }
+}
+
+// Stages of the TMA-fed kernel: 2..kMaxOutStages groups of A1 x 128 floats
+// within ~64 KB; 0 = plain kernel.  Measured (ncu, isolated kernels): the TMA
+// ring wins when a thread has many points to load (c5, A1 = 64: 55.7 -> 49.5
+// us) and loses when the groups are small (c2, A1 = 6: 28 -> 32 us; c3,
+// A1 = 16: 0.55 -> 0.65 ms), where the per-group barrier and refill cost
+// more than the plain loads' latency: TMA for A1 >= 32.
+template <int N, int A>
+constexpr int out_stages() {
+  constexpr int A1 = ipow(A, N - 1);
+  constexpr int bytes = A1 * 128 * 4;
+  constexpr int n = (64 * 1024) / bytes;
+  return (A1 < 32 || A1 > 256) ? 0 : n >= kMaxOutStages ? kMaxOutStages : n >= 2 ? n : 0;
+}
+
+template <int N, int A, int M, class Tab>
+cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams& xp, const CUtensorMap* tmM,
+                       cudaStream_t s) {
+  constexpr int ns = out_stages<N, A>();
+  if constexpr (ns > 0) {
+    if (tmM) {
+      auto kern = k_output_xform_tma<N, A, M, Tab>;
+      constexpr int smem = ns * ipow(A, N - 1) * 128 * 4;
+      static int grid_per_sm = 0, sms = 0;
+      if (!grid_per_sm) {
+        if (smem > 46 * 1024) {
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (e != cudaSuccess) return e;
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, kern, 128, smem) != cudaSuccess ||
+            grid_per_sm < 1)
+          grid_per_sm = 1;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+      }
+      const int64_t nunits = ((g.T - g.t_beg + 127) / 128) * (int64_t)g.K;
+      int64_t grid = (int64_t)grid_per_sm * sms;
+      if (grid > nunits) grid = nunits;
+      return launch_pdl(kern, dim3((unsigned)grid), dim3(128), smem, s, y, g, xp, *tmM, ns);
+    }
+  }
   dim3 grid((unsigned)((g.T - g.t_beg + 127) / 128), (unsigned)g.K);
   return launch_pdl(k_output_xform<N, A, M, Tab>, grid, dim3(128), 0, s, Mx, y, g, xp);
 }
 
 template <int A, int M, class Tab>
-cudaError_t launch_out_byN(int N, const float* Mx, float* y, const KGeom& g, const XfParams& xp, cudaStream_t s) {
+cudaError_t launch_out_byN(int N, const float* Mx, float* y, const KGeom& g, const XfParams& xp,
+                           const CUtensorMap* tmM, cudaStream_t s) {
   switch (N) {
-    case 1: return launch_out<1, A, M, Tab>(Mx, y, g, xp, s);
-    case 2: return launch_out<2, A, M, Tab>(Mx, y, g, xp, s);
-    case 3: return launch_out<3, A, M, Tab>(Mx, y, g, xp, s);
+    case 1: return launch_out<1, A, M, Tab>(Mx, y, g, xp, tmM, s);
+    case 2: return launch_out<2, A, M, Tab>(Mx, y, g, xp, tmM, s);
+    case 3: return launch_out<3, A, M, Tab>(Mx, y, g, xp, tmM, s);
     case 4:
-      if constexpr (ipow(A, 3) <= 64) return launch_out<4, A, M, Tab>(Mx, y, g, xp, s);
+      if constexpr (ipow(A, 3) <= 64) return launch_out<4, A, M, Tab>(Mx, y, g, xp, tmM, s);
       else return cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
   }
@@ -125,8 +254,8 @@ cudaError_t launch_out_byN(int N, const float* Mx, float* y, const KGeom& g, con
 }  // namespace out_detail
 
 cudaError_t launch_output_const(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
-                                const XfParams& xp, cudaStream_t s);
+                                const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
 cudaError_t launch_output_run(int N, int alpha, int m, const float* Mx, float* y, const KGeom& g,
-                              const XfParams& xp, cudaStream_t s);
+                              const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
 
 }  // namespace wino

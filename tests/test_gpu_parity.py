@@ -205,6 +205,25 @@ def test_input_cp_async_fallback_matches_tma(name, monkeypatch):
     assert torch.equal(y_tma, y_cp)
 
 
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_output_tma_ring_matches_plain(name, monkeypatch):
+    # a4 reading M through the TMA ring (alpha^(N-1) >= 32) and through plain
+    # per-thread loads: same arithmetic, same bits; also with the L2-chunked
+    # pipeline (M rows relative to the chunk) and with several samples per
+    # t-block boundary (ragged T)
+    cfg = SMALL[name]
+    y_tma, _ = _run_env(cfg, monkeypatch)
+    y_ld, _ = _run_env(cfg, monkeypatch, WINO_OUT_TMA="0")
+    assert torch.equal(y_tma, y_ld)
+    x, g = make_inputs(cfg)
+    monkeypatch.setenv("WINO_CHUNK_MB", "0.05")
+    plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, cfg.batch, cfg.padding, fuse=4)
+    assert plan.info["chunk_slabs"] > 0
+    plan.filter_transform(g.cuda())
+    assert torch.equal(plan.forward(x.cuda()).cpu(), y_tma)
+    plan.close()
+
+
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 @pytest.mark.parametrize("chunk_mb", ["0.05", "1"])
 def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
