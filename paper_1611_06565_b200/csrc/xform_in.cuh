@@ -223,8 +223,26 @@ struct PlaneInfo {
 template <int N, int A, int M, class Tab, int D>
 __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int slab_f, float* __restrict__ H,
                                                  float* __restrict__ V, const KGeom& g, const XfParams& xp,
-                                                 const PlaneInfo* pl, int npl) {
+                                                 const PlaneInfo* pl, int npl, uint32_t mb0) {
   const int64_t pstride = (int64_t)g.C * g.T_s;
+  // slab p's TMA box has landed once its mbarrier completes phase 0; every
+  // thread waits only for the slabs of its own items, in order, so work on
+  // the first slab starts while the next ones are still in flight
+  int landed = -1;
+  auto ensure = [&](int p) {
+    if (mb0 == 0u) return;
+    while (landed < p) {
+      ++landed;
+      uint32_t done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+            : "=r"(done)
+            : "r"(mb0 + 8u * landed)
+            : "memory");
+      }
+    }
+  };
   auto vbase = [&](int p) -> float* {
     return V + (int64_t)pl[p].c * g.T_s + ((int64_t)pl[p].b * g.Tps + (int64_t)pl[p].a0 * g.R - g.t0);
   };
@@ -240,6 +258,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // consecutive x, conflict-free)
       for (int r = warp; r < npl * e1; r += nwarps) {
         const int p = r / e1, y = r - p * e1;
+        ensure(p);
         float* row = S0 + p * slab_f + y * g.sst[1] + D;
         for (int xh = lane; xh < e2; xh += 32) {
           float* col = row + xh;
@@ -285,6 +304,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       return;
     }
     // separate H buffer (npl = 1): H = [t0][xi_0][y][x], window rows 16-byte aligned
+    ensure(0);
     const PlaneInfo& q = pl[0];
     const int hp = g.hpitch, nt0 = q.nt0;
     // phase 1: one thread per (t0, y, x) column: alpha values along axis 0
@@ -336,6 +356,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     constexpr int NX = N >= 3 ? A : 1;        // work items per tile (one per xi_0 when N >= 3)
     if (npl == 1) {
       // one plane: no plane index to decode (the common case for large slabs)
+      ensure(0);
       const int ntile = pl[0].nt0 * g.R;
       float* __restrict__ vb = vbase(0);
       for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
@@ -361,6 +382,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       const int xi0 = w / ntile;
       const int tl = w - xi0 * ntile;
       if (tl >= pl[p].nt0 * g.R) continue;    // last axis-0 box of a sample is shorter
+      ensure(p);
       // local tile -> slab offset of its window
       int rem = tl, base = 0;
 #pragma unroll
@@ -417,16 +439,6 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
       }
     }
     __syncthreads();
-    for (int p = 0; p < npl; ++p) {
-      uint32_t done = 0;
-      while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(mb0 + 8u * p)
-            : "memory");
-      }
-    }
   } else {
     static_assert(D == 0, "the cp.async slab path is unshifted");
     __syncthreads();
@@ -434,7 +446,8 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
       load_slab_cpasync<N, A, M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c);
     __syncthreads();
   }
-  transform_planes<N, A, M, Tab, D>(smem_f, slab_f, H, V, g, xp, pl, npl);
+  transform_planes<N, A, M, Tab, D>(smem_f, slab_f, H, V, g, xp, pl, npl,
+                                    kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u);
 }
 
 template <class K>
