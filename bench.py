@@ -56,6 +56,8 @@ def parse_args():
     ap.add_argument("--fuse", type=int, default=0, help="plan fuse bitmask (4 = L2-chunked a2->a3->a4)")
     ap.add_argument("--nets", default="fig4_f54,fig4_f34,fig3_f54",
                     help="the paper's own 2-D workloads (Figures 3 and 4) to time at N=1 ('' for none)")
+    ap.add_argument("--nd", default="c3t",
+                    help="per-axis F(m_1 x .. , r_1 x ..) workloads to time at N=1 ('' for none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
     return ap.parse_args()
@@ -329,6 +331,64 @@ def run_nets(args, local):
     return out
 
 
+# Per-axis workloads (NEXT-2): c3's video layer with F(2,3) along time and
+# F(4,3) along space (Eq. (4)'s per-axis transforms)
+ND_WORKLOADS = {
+    "c3t": dict(N=3, dims=(16, 56, 56), m=(2, 4, 4), r=(3, 3, 3), pad=(1, 1, 1), B=16, C=64, K=128,
+                desc="c3 video layer 16x56x56, 16x64->128, F(2,3) time x F(4x4,3x3) space"),
+}
+
+
+def run_nd(args, local):
+    import torch
+    import paper_1611_06565_b200 as pkg
+    dev = torch.device("cuda", local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sink = torch.empty((), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    steps = max(3, min(args.steps, 20))
+    out = {}
+    for name in [n for n in args.nd.split(",") if n]:
+        w = ND_WORKLOADS[name]
+        gen = torch.Generator("cpu").manual_seed(0)
+        x = torch.randn((w["B"], w["C"]) + w["dims"], generator=gen)
+        g = torch.randn((w["K"], w["C"]) + w["r"], generator=gen) * math.sqrt(2.0 / (w["C"] * math.prod(w["r"])))
+        plan = pkg.Plan(w["N"], w["dims"], list(w["m"]), list(w["r"]), w["C"], w["K"], w["B"], w["pad"],
+                        device=local)
+        plan.filter_transform(g.to(dev), stream)
+        xd = x.to(dev)
+        y = torch.empty((w["B"], w["K"]) + tuple(plan.out_dims), device=dev)
+        for _ in range(max(args.warmup, 3)):
+            plan.forward(xd, y, stream)
+        torch.cuda.synchronize(dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            flush.zero_()
+            torch.sum(flush.view(torch.int64), dim=0, out=sink)
+            a.record(stream)
+            plan.forward(xd, y, stream)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+        plan.profile(True)
+        for _ in range(3):
+            plan.forward(xd, y, stream)
+        torch.cuda.synchronize(dev)
+        stage_ms, calls = plan.profile_read()
+        plan.profile(False)
+        flops = 2 * w["B"] * w["K"] * w["C"] * math.prod(plan.out_dims) * math.prod(w["r"])
+        out[name] = {"desc": w["desc"], "F": "F(%s, %s)" % ("x".join(map(str, w["m"])), "x".join(map(str, w["r"]))),
+                     "ms_per_layer": round(ms, 4), "tflops_direct_equiv": round(flops / (ms * 1e-3) / 1e12, 2),
+                     "n_points": plan.info["n_points"],
+                     "stages_ms": {s: round(v / calls, 4) for s, v in
+                                   zip(["input_xform", "gemm", "output_xform"], stage_ms)},
+                     "path": "generic multi-pass per-axis transforms (xform_nd.cu) + tcgen05 3xTF32 GEMM"}
+        plan.close()
+        del xd, y
+        torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline_sample(cfg, seconds):
     """Time the float64 oracle (as it stands) on a bounded sample of the
     workload: outputs computed one by one at random positions."""
@@ -442,6 +502,8 @@ def main():
         out["configs"] = configs
         if world == 1 and args.nets:
             out["paper_workloads"] = run_nets(args, local)
+        if world == 1 and args.nd:
+            out["per_axis_workloads"] = run_nd(args, local)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -108,6 +108,18 @@ WINO_API wino_status wino_plan_create_ex(wino_plan_t* plan, int N, const int64_t
                                 int C, int K, int batch, const int* padding, const char* points,
                                 int gemm_mode, int fuse, int device);
 
+/* Per-axis transforms F(m_1 x .. x m_N, r_1 x .. x r_N): Eq. (4) indexes A_n,
+ * B_n, C_n by axis, e.g. F(2,3) along time and F(4,3)
+ * along space, or anisotropic kernels r = (1,3,3).  m[0..N), r[0..N) >= 1
+ * with alpha_n = m_n + r_n - 1 <= 8 and prod alpha_n <= 65535; default
+ * points per alpha_n; g is [K][C][r_1]..[r_N].  Equal (m_n, r_n) on every
+ * axis returns the plan of wino_plan_create_ex (fused kernels); otherwise the
+ * plan runs generic multi-pass transforms around the same GEMM (no fusion
+ * bitmask).  Errors as wino_plan_create_ex. */
+WINO_API wino_status wino_plan_create_nd(wino_plan_t* plan, int N, const int64_t* dims, const int* m,
+                                         const int* r, int C, int K, int batch, const int* padding,
+                                         int gemm_mode, int device);
+
 /* Frees every device/host buffer of the plan.  The caller must ensure no work
  * using the plan is still in flight (synchronise first).  NULL is a no-op. */
 WINO_API wino_status wino_plan_destroy(wino_plan_t plan);

@@ -8,7 +8,7 @@ step, over exact ``Fraction`` (object arrays) or float64:
    ceil(out/S) tiles per axis, tile t reads input [tS - P, tS - P + D)
    zero-filled, outputs past `out` discarded);
 2. kernel transform  G x_{n=1}^N C_n   (Eq. (4)),
-   data transform    D x_{n=1}^N B_n,
+   data transform    D x_{n=1}^N B_n  (one F(S_n, G_n) per axis allowed),
    each a chain of n-mode products (Eq. (3), PAPER.md:150-154);
 3. per transform point i: S_hat^(i) = D_hat^(i) x G_hat^(i) with D_hat T x M
    (tiles-by-channels) and G_hat M x K (Eq. (5)) -- the
@@ -45,24 +45,32 @@ def multi_mode_product(X: np.ndarray, U: np.ndarray, axes) -> np.ndarray:
     return X
 
 
-def tile_geometry(in_dims, r: int, m: int, pad):
-    """out dims, tiles per axis, T per sample (readings #2, #10)."""
-    out = tuple(int(i) + 2 * int(p) - r + 1 for i, p in zip(in_dims, pad))
-    tiles = tuple(math.ceil(o / m) for o in out)
+def _per_axis(v, N):
+    """An int or a length-N sequence -> tuple of N ints."""
+    return tuple(int(a) for a in v) if isinstance(v, (list, tuple)) else (int(v),) * N
+
+
+def tile_geometry(in_dims, r, m, pad):
+    """out dims, tiles per axis, T per sample (readings #2, #10); r and m may
+    be per-axis sequences (Eq. (4) indexes the transforms by axis n)."""
+    N = len(in_dims)
+    r, m = _per_axis(r, N), _per_axis(m, N)
+    out = tuple(int(i) + 2 * int(p) - rn + 1 for i, p, rn in zip(in_dims, pad, r))
+    tiles = tuple(math.ceil(o / mn) for o, mn in zip(out, m))
     return out, tiles
 
 
-def extract_tiles(x: np.ndarray, m: int, alpha: int, pad, zero):
-    """x [B][C][in...] -> tiles [B][C][t_1..t_N][alpha]*N, zero-filled."""
+def extract_tiles(x: np.ndarray, m, alpha, pad, zero):
+    """x [B][C][in...] -> tiles [B][C][t_1..t_N][alpha_1..alpha_N], zero-filled."""
     N = x.ndim - 2
-    B, C = x.shape[:2]
-    r = alpha - m + 1
+    m, alpha = _per_axis(m, N), _per_axis(alpha, N)
+    r = tuple(a - mn + 1 for a, mn in zip(alpha, m))
     out, tiles = tile_geometry(x.shape[2:], r, m, pad)
-    res = np.empty((B, C) + tiles + (alpha,) * N, dtype=x.dtype)
+    res = np.empty(x.shape[:2] + tiles + alpha, dtype=x.dtype)
     res[...] = zero
     for tidx in np.ndindex(*tiles):
-        for w in np.ndindex(*((alpha,) * N)):
-            src = tuple(tidx[n] * m - pad[n] + w[n] for n in range(N))
+        for w in np.ndindex(*alpha):
+            src = tuple(tidx[n] * m[n] - pad[n] + w[n] for n in range(N))
             if all(0 <= src[n] < x.shape[2 + n] for n in range(N)):
                 res[(slice(None), slice(None)) + tidx + w] = x[(slice(None), slice(None)) + src]
     return res, out, tiles
@@ -70,14 +78,13 @@ def extract_tiles(x: np.ndarray, m: int, alpha: int, pad, zero):
 
 def winograd_nd(x, g, pad, A, B, C, exact: bool = False):
     """Full N-D Winograd layer.  Returns (y, stages) where stages holds
-    U [alpha^N][M][K] (G_hat^(i)), V [alpha^N][T][M] (D_hat^(i)),
-    Shat [alpha^N][T][K] (S_hat^(i)), with i row-major over the D^N
-    transform-domain coordinates and t row-major over (b, t_1..t_N)."""
-    A_ = as_array(A, exact)
-    B_ = as_array(B, exact)
-    C_ = as_array(C, exact)
-    S, D = A_.shape
-    Gk = C_.shape[1]
+    U [P][M][K] (G_hat^(i)), V [P][T][M] (D_hat^(i)), Shat [P][T][K]
+    (S_hat^(i)), P = prod_n D_n, with i row-major over the transform-domain
+    coordinates and t row-major over (b, t_1..t_N).
+
+    A, B, C are one matrix each (the same F(S, G) on every axis) or lists of
+    N matrices A_n (S_n x D_n), B_n (D_n x D_n), C_n (D_n x G_n): Eq. (4)
+    applies x_n with the n-th transform."""
     if exact:
         x = np.asarray(x, dtype=object)
         g = np.asarray(g, dtype=object)
@@ -87,19 +94,34 @@ def winograd_nd(x, g, pad, A, B, C, exact: bool = False):
         g = np.asarray(g, dtype=np.float64)
         zero = 0.0
     N = x.ndim - 2
+
+    def axes_list(Mx):
+        # a single matrix (list of rows of scalars) or a list of N matrices
+        if isinstance(Mx, (list, tuple)) and len(Mx) == N and np.ndim(np.asarray(Mx[0], dtype=object)) == 2:
+            return [as_array(Mi, exact) for Mi in Mx]
+        return [as_array(Mx, exact)] * N
+
+    As, Bs, Cs = axes_list(A), axes_list(B), axes_list(C)
+    S = tuple(a.shape[0] for a in As)
+    D = tuple(a.shape[1] for a in As)
+    Gk = tuple(c.shape[1] for c in Cs)
     if np.isscalar(pad):
         pad = (int(pad),) * N
     Bn, M = x.shape[:2]
     K = g.shape[0]
-    assert g.shape[2:] == (Gk,) * N
+    assert g.shape[2:] == Gk
 
-    # (2) kernel transform: G x_{n=1}^N C  -> [K][M][D..D]
-    Ug = multi_mode_product(g, C_, range(2, 2 + N))
-    # (1)+(2) tiles and data transform: D x_{n=1}^N B
+    # (2) kernel transform: G x_{n=1}^N C_n  -> [K][M][D_1..D_N]
+    Ug = g
+    for n in range(N):
+        Ug = nmode_product(Ug, Cs[n], 2 + n)
+    # (1)+(2) tiles and data transform: D x_{n=1}^N B_n
     tiles, out, tgrid = extract_tiles(x, S, D, pad, zero)
-    Vt = multi_mode_product(tiles, B_, range(2 + N, 2 + 2 * N))   # [B][M][tiles][D..]
+    Vt = tiles
+    for n in range(N):
+        Vt = nmode_product(Vt, Bs[n], 2 + N + n)                   # [B][M][tiles][D..]
     T = Bn * int(np.prod(tgrid))
-    P = D ** N
+    P = int(np.prod(D))
     # i-major matrices of Eq. (5)
     Ghat = Ug.reshape(K, M, P).transpose(2, 1, 0)                     # [P][M][K]
     Dhat = np.moveaxis(Vt, 1, -1 - N)                                 # [B][tiles][M][D..]
@@ -109,14 +131,15 @@ def winograd_nd(x, g, pad, A, B, C, exact: bool = False):
     for i in range(P):
         Shat[i] = np.dot(Dhat[i], Ghat[i])
     # (4) inverse transform per (t, k) and stitch
-    St = Shat.transpose(1, 2, 0).reshape((T, K) + (D,) * N)
-    Yt = multi_mode_product(St, A_, range(2, 2 + N))                  # [T][K][S..S]
-    Yt = Yt.reshape((Bn,) + tgrid + (K,) + (S,) * N)
+    Yt = Shat.transpose(1, 2, 0).reshape((T, K) + D)
+    for n in range(N):
+        Yt = nmode_product(Yt, As[n], 2 + n)                          # [T][K][S..]
+    Yt = Yt.reshape((Bn,) + tgrid + (K,) + S)
     y = np.empty((Bn, K) + out, dtype=Dhat.dtype)
     for b in range(Bn):
         for tidx in np.ndindex(*tgrid):
-            for o in np.ndindex(*((S,) * N)):
-                dst = tuple(tidx[n] * S + o[n] for n in range(N))
+            for o in np.ndindex(*S):
+                dst = tuple(tidx[n] * S[n] + o[n] for n in range(N))
                 if all(dst[n] < out[n] for n in range(N)):
                     y[(b, slice(None)) + dst] = Yt[(b,) + tidx + (slice(None),) + o]
     return y, {"U": Ghat, "V": Dhat, "Shat": Shat, "out": out, "tiles": tgrid}

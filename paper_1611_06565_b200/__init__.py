@@ -13,12 +13,12 @@ and hand-written sm_100a kernels behind the C ABI of include/wino.h.
 from .net import Net
 from .wino import (Plan, WinoError, wino_filter_buffer, wino_filter_mark_ready, wino_filter_transform,
                    wino_forward, wino_forward_ex, wino_forward_host, wino_get_transforms, wino_last_error, wino_plan_create,
-                   wino_plan_create_ex, wino_plan_destroy, wino_plan_info, wino_plan_out_dims,
+                   wino_plan_create_ex, wino_plan_create_nd, wino_plan_destroy, wino_plan_info, wino_plan_out_dims,
                    wino_plan_sizes, wino_profile_enable, wino_profile_read, wino_synthesize, wino_version,
                    wino_workspace, WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32,
                    WINO_ACT_NONE, WINO_ACT_RELU)
 
-__all__ = ["Plan", "Net", "WinoError", "wino_plan_create", "wino_plan_create_ex", "wino_plan_destroy",
+__all__ = ["Plan", "Net", "WinoError", "wino_plan_create", "wino_plan_create_ex", "wino_plan_create_nd", "wino_plan_destroy",
            "wino_filter_transform", "wino_forward", "wino_forward_ex", "wino_forward_host", "wino_plan_out_dims",
            "wino_plan_sizes", "wino_plan_info", "wino_filter_buffer", "wino_filter_mark_ready",
            "wino_workspace", "wino_profile_enable", "wino_profile_read", "wino_synthesize",

@@ -70,11 +70,20 @@ struct XfParams {
   float BT[kMaxA][kMaxA];
 };
 
-// Tables for the filter transform (fp64).
+// Tables for the filter transform (fp64), one G per axis (axis n: a[n] x r[n]).
 struct FParams {
-  double G[kMaxA][kMaxA];
-  int N, a, r, C, K, K_s;
-  int64_t P;  // a^N
+  double G[kMaxN][kMaxA][kMaxA];
+  int a[kMaxN], r[kMaxN];
+  int N, C, K, K_s;
+  int64_t P;  // prod_n a[n]
+};
+
+// Per-axis transforms of an N-D plan with different (m_n, r_n) per axis
+// (Eq. (4) indexes B_n, A_n by n; xform_nd.cu).
+struct NdParams {
+  float BT[kMaxN][kMaxA][kMaxA];  // axis n: a[n] x a[n]
+  float AT[kMaxN][kMaxA][kMaxA];  // axis n: m[n] x a[n]
+  int a[kMaxN], m[kMaxN];
 };
 
 // Table providers.  ConstTab<M, R, PS>: tables synthesised at compile time

@@ -23,6 +23,11 @@ cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x
 bool encode_output_map(CUtensorMap* tm, const float* Mx, int64_t T_s, int K, int64_t P, int A1);
 cudaError_t launch_output_xform(int N, int alpha, int m, int spec, const float* Mx, float* y, const KGeom& g,
                                 const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
+// per-axis (m_n, r_n) plans (xform_nd.cu): multi-pass a2 / a4 over tiles [t_lo, t_hi)
+cudaError_t launch_input_nd(const float* x, float* V, const KGeom& g, const NdParams& q, int N, int64_t P,
+                            int64_t t_lo, int64_t t_hi, cudaStream_t s);
+cudaError_t launch_output_nd(const float* Mx, float* W, float* y, const KGeom& g, const NdParams& q, int N,
+                             int64_t t_lo, int64_t t_hi, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s);
 

@@ -198,6 +198,12 @@ struct wino_plan_s {
   // of chunk_slabs input slabs (rows t - t_lo), sized to stay L2-resident
   bool chunked = false;
   int64_t chunk_slabs = 0;
+  // per-axis (m_n, r_n) plan (wino_plan_create_nd with unequal axes):
+  // generic multi-pass transforms (xform_nd.cu), scratch W for the output passes
+  bool nd = false;
+  int mn[kMaxN]{}, rn[kMaxN]{}, an[kMaxN]{};
+  NdParams ndp{};
+  float* W = nullptr;
   bool prof = false;
   int prof_calls = 0;
   std::vector<cudaEvent_t> ev;  // pool; prof_stage[i] tags pair (2i, 2i+1)
@@ -284,9 +290,10 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
     for (int j = 0; j < kMaxA; ++j) {
       p->xp.AT[i][j] = ft.AT[i][j];
       p->xp.BT[i][j] = ft.BT[i][j];
-      p->fp.G[i][j] = ft.G[i][j];
+      for (int n = 0; n < kMaxN; ++n) p->fp.G[n][i][j] = ft.G[i][j];
     }
-  p->fp.N = N; p->fp.a = a; p->fp.r = r; p->fp.C = C; p->fp.K = K; p->fp.K_s = (int)p->K_s; p->fp.P = p->P;
+  for (int n = 0; n < kMaxN; ++n) { p->fp.a[n] = a; p->fp.r[n] = r; }
+  p->fp.N = N; p->fp.C = C; p->fp.K = K; p->fp.K_s = (int)p->K_s; p->fp.P = p->P;
 
   KGeom& g = p->geom;
   int64_t sin = 1, sout = 1;
@@ -382,6 +389,119 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   return WINO_OK;
 }
 
+wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
+                                int C, int K, int batch, const int* padding, int gemm_mode, int device) {
+  if (!plan_out) return fail(WINO_ERR_ARG, "plan pointer is NULL");
+  *plan_out = nullptr;
+  if (N < 1 || N > kMaxN) return fail(WINO_ERR_ARG, "N must be in 1..4 (got %d)", N);
+  if (!dims || !m || !r) return fail(WINO_ERR_ARG, "dims, m or r is NULL");
+  if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
+  if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
+  bool uniform = true;
+  for (int n = 1; n < N; ++n) uniform = uniform && m[n] == m[0] && r[n] == r[0];
+  // equal axes: the single-(m, r) plan and its fused kernels
+  if (uniform) return wino_plan_create_ex(plan_out, N, dims, m[0], r[0], C, K, batch, padding, nullptr, gemm_mode, 0,
+                                          device);
+  Transforms tn[kMaxN];
+  int64_t P = 1;
+  for (int n = 0; n < N; ++n) {
+    int spec;
+    wino_status st = synth_checked(m[n], r[n], nullptr, tn[n], spec);
+    if (st) return st;
+    if (tn[n].a > kMaxA)
+      return fail(WINO_ERR_UNSUPPORTED, "alpha_%d = m + r - 1 = %d exceeds %d on the device path", n, tn[n].a, kMaxA);
+    P *= tn[n].a;
+  }
+  wino_plan_s* p = new wino_plan_s();
+  p->nd = true;
+  p->N = N; p->m = m[0]; p->r = r[0]; p->a = tn[0].a; p->C = C; p->K = K; p->batch = batch;
+  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? WINO_GEMM_3XTF32 : gemm_mode;
+  p->spec = kSpecRuntime;
+  p->use_tma_in = false;
+  p->tf = tn[0];
+  int64_t Tps = 1;
+  for (int n = 0; n < N; ++n) {
+    p->mn[n] = m[n]; p->rn[n] = r[n]; p->an[n] = tn[n].a;
+    p->in[n] = dims[n];
+    p->pad[n] = padding ? padding[n] : 0;
+    if (dims[n] < 1 || p->pad[n] < 0) { delete p; return fail(WINO_ERR_ARG, "dims must be >= 1 and padding >= 0"); }
+    p->out[n] = dims[n] + 2 * p->pad[n] - r[n] + 1;
+    if (p->out[n] < 1) { delete p; return fail(WINO_ERR_SHAPE, "kernel %d larger than padded input %lld on axis %d", r[n], (long long)(dims[n] + 2 * p->pad[n]), n); }
+    p->tiles[n] = (int)((p->out[n] + m[n] - 1) / m[n]);
+    Tps *= p->tiles[n];
+  }
+  p->Tps = Tps;
+  const int64_t T = Tps * batch;
+  if (T > (int64_t)INT32_MAX - 256) { delete p; return fail(WINO_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)T); }
+  p->T_s = (T + 127) / 128 * 128;
+  p->P = P;
+  if (P > 65535) { delete p; return fail(WINO_ERR_UNSUPPORTED, "prod alpha_n = %lld points exceeds 65535", (long long)P); }
+  const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32;
+  const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+  p->K_s = tc ? (K + bn - 1) / bn * bn : (K + 31) / 32 * 32;
+  // per-axis tables: B_n^T, A_n^T (fp32, RNE from exact), G_n (fp64)
+  for (int n = 0; n < kMaxN; ++n) {
+    const FloatTables ft = to_tables(tn[n < N ? n : 0]);
+    for (int i = 0; i < kMaxA; ++i)
+      for (int j = 0; j < kMaxA; ++j) {
+        p->ndp.BT[n][i][j] = ft.BT[i][j];
+        p->ndp.AT[n][i][j] = ft.AT[i][j];
+        p->fp.G[n][i][j] = ft.G[i][j];
+      }
+    p->ndp.a[n] = n < N ? tn[n].a : 1;
+    p->ndp.m[n] = n < N ? m[n] : 1;
+    p->fp.a[n] = n < N ? tn[n].a : 1;
+    p->fp.r[n] = n < N ? r[n] : 1;
+  }
+  p->fp.N = N; p->fp.C = C; p->fp.K = K; p->fp.K_s = (int)p->K_s; p->fp.P = P;
+  KGeom& g = p->geom;
+  int64_t sin = 1, sout = 1;
+  for (int n = N - 1; n >= 0; --n) {
+    g.in[n] = p->in[n]; g.out[n] = p->out[n]; g.tiles[n] = p->tiles[n]; g.pad[n] = p->pad[n];
+    g.in_stride[n] = sin; g.out_stride[n] = sout;
+    sin *= p->in[n]; sout *= p->out[n];
+  }
+  g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m[0];
+  if (device < 0) {
+    if (cudaGetDevice(&device) != cudaSuccess) { delete p; return fail(WINO_ERR_CUDA, "no CUDA device"); }
+  }
+  p->device = device;
+  DeviceGuard guard(device);
+  const size_t ucount = (size_t)P * C * p->K_s;
+  const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
+  p->filter_bytes = ucount * 4 * nbuf;
+  p->ws_bytes = ((size_t)P * C * p->T_s + (size_t)P * K * p->T_s) * 4;
+  cudaError_t e = cudaMalloc(&p->ubuf, p->filter_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->V, p->ws_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&p->W, (size_t)P * K * p->T_s * 4);
+  if (e == cudaSuccess) e = cudaMemset(p->V, 0, p->ws_bytes);
+  if (e != cudaSuccess) {
+    wino_plan_destroy(p);
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? WINO_ERR_NOMEM : WINO_ERR_CUDA, "device allocation failed: %s",
+                cudaGetErrorString(e));
+  }
+  p->M = p->V + (size_t)P * C * p->T_s;
+  if (p->gemm_mode == WINO_GEMM_FFMA) {
+    p->U32 = p->ubuf;
+  } else {
+    p->Uhi = p->ubuf;
+    p->Ulo = p->ubuf + ucount;
+  }
+  p->filter_bcast_bytes = p->filter_bytes;
+  if (tc) {
+    e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)P, p->T_s, C, (int)p->K_s, K,
+                        p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
+    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)P, T, p->T_s, C, K);
+    if (e != cudaSuccess) {
+      wino_plan_destroy(p);
+      return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *plan_out = p;
+  return WINO_OK;
+}
+
 wino_status wino_plan_create(wino_plan_t* plan, int N, const int64_t* dims, int m, int r, int C, int K, int batch,
                              const int* padding) {
   return wino_plan_create_ex(plan, N, dims, m, r, C, K, batch, padding, nullptr, WINO_GEMM_AUTO, 0, -1);
@@ -394,6 +514,7 @@ wino_status wino_plan_destroy(wino_plan_t p) {
   cudaFree(p->V);
   cudaFree(p->x_dev);
   cudaFree(p->y_dev);
+  cudaFree(p->W);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   if (p->s_in) {
     for (int i = 0; i < kHostChunks; ++i) {
@@ -452,6 +573,31 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
   g.bias = bias;
   g.act = act;
   const bool rec = p->prof && p->prof_calls < kMaxProf;
+  if (p->nd) {
+    // per-axis plan: generic multi-pass transforms around the same GEMM
+    const int64_t T = (int64_t)B * p->Tps;
+    g.T = T;
+    g.t0 = 0;
+    g.t_beg = 0;
+    ProfScope ps{p, s, 0};
+    if (rec) CUDA_TRY(ps.begin());
+    CUDA_TRY(launch_input_nd(x, p->V, g, p->ndp, p->N, p->P, 0, T, s));
+    if (rec) CUDA_TRY(ps.end());
+    ProfScope pg{p, s, 1};
+    if (rec) CUDA_TRY(pg.begin());
+    if (p->gemm_mode == WINO_GEMM_FFMA) {
+      CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, T, p->T_s, p->C, p->K, (int)p->K_s, s));
+    } else {
+      CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, 0, T, p->T_s, p->C, p->K, s));
+    }
+    if (rec) CUDA_TRY(pg.end());
+    ProfScope po{p, s, 2};
+    if (rec) CUDA_TRY(po.begin());
+    CUDA_TRY(launch_output_nd(p->M, p->W, y, g, p->ndp, p->N, 0, T, s));
+    if (rec) CUDA_TRY(po.end());
+    if (rec) ++p->prof_calls;
+    return WINO_OK;
+  }
   // TMA map of x, re-encoded when the input pointer or batch changes
   if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
     p->tm_x_ok = encode_input_map(&p->tm_x, x, g, p->N, B);

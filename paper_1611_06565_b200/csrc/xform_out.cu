@@ -9,7 +9,7 @@ namespace wino {
 
 // ------------------------------------------------------------------ a1
 // One thread per (xi, c, k) (k fastest -> coalesced U writes):
-//   U_xi[c][k] = sum_p prod_n G[xi_n][p_n] g[k, c, p]
+//   U_xi[c][k] = sum_p prod_n G_n[xi_n][p_n] g[k, c, p]   (G_n per axis)
 // in fp64, rounded once to fp32, then split for 3xTF32:
 //   hi = rna_tf32(u), lo = rna_tf32(u - hi)     (reading #7).
 __global__ void __launch_bounds__(256)
@@ -24,16 +24,16 @@ k_filter_xform(const float* __restrict__ g, float* __restrict__ Uhi, float* __re
   float u = 0.f;
   if (k < fp.K) {
     int rN = 1;
-    for (int n = 0; n < fp.N; ++n) rN *= fp.r;
+    for (int n = 0; n < fp.N; ++n) rN *= fp.r[n];
     const float* gk = g + ((int64_t)k * fp.C + c) * rN;
     int xd[kMaxN];
     int64_t q = xi;
-    for (int n = fp.N - 1; n >= 0; --n) { xd[n] = (int)(q % fp.a); q /= fp.a; }
+    for (int n = fp.N - 1; n >= 0; --n) { xd[n] = (int)(q % fp.a[n]); q /= fp.a[n]; }
     double acc = 0.0;
     for (int p = 0; p < rN; ++p) {
       double w = 1.0;
       int pq = p;
-      for (int n = fp.N - 1; n >= 0; --n) { w *= fp.G[xd[n]][pq % fp.r]; pq /= fp.r; }
+      for (int n = fp.N - 1; n >= 0; --n) { w *= fp.G[n][xd[n]][pq % fp.r[n]]; pq /= fp.r[n]; }
       if (w != 0.0) acc = fma(w, (double)__ldg(gk + p), acc);
     }
     u = (float)acc;

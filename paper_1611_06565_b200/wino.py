@@ -30,7 +30,7 @@ WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32 = 0, 1, 2, 3
 WINO_FUSE_NONE, WINO_FUSE_L2_CHUNK = 0, 4
 WINO_ACT_NONE, WINO_ACT_RELU = 0, 1
 
-EXPORTS = ["wino_plan_create", "wino_plan_create_ex", "wino_plan_destroy", "wino_filter_transform",
+EXPORTS = ["wino_plan_create", "wino_plan_create_ex", "wino_plan_create_nd", "wino_plan_destroy", "wino_filter_transform",
            "wino_forward", "wino_forward_ex", "wino_forward_host", "wino_plan_out_dims", "wino_plan_sizes",
            "wino_plan_info", "wino_filter_buffer", "wino_filter_mark_ready", "wino_workspace",
            "wino_profile_enable", "wino_profile_read", "wino_synthesize", "wino_get_transforms",
@@ -61,6 +61,8 @@ def lib() -> ctypes.CDLL:
             "wino_plan_create": [ctypes.POINTER(vp), c_int, i64p, c_int, c_int, c_int, c_int, c_int, i32p],
             "wino_plan_create_ex": [ctypes.POINTER(vp), c_int, i64p, c_int, c_int, c_int, c_int, c_int,
                                     i32p, ctypes.c_char_p, c_int, c_int, c_int],
+            "wino_plan_create_nd": [ctypes.POINTER(vp), c_int, i64p, i32p, i32p, c_int, c_int, c_int, i32p,
+                                    c_int, c_int],
             "wino_plan_destroy": [vp],
             "wino_filter_transform": [vp, vp, vp],
             "wino_forward": [vp, vp, vp, c_int, vp],
@@ -147,6 +149,17 @@ def wino_plan_create_ex(N, dims, m, r, C, K, batch, padding=None, points=None, g
     _check(lib().wino_plan_create_ex(ctypes.byref(h), int(N), _i64arr(dims), int(m), int(r), int(C),
                                      int(K), int(batch), pad, points.encode() if points else None,
                                      int(gemm_mode), int(fuse), int(device)))
+    return h.value
+
+
+def wino_plan_create_nd(N, dims, m, r, C, K, batch, padding=None, gemm_mode=0, device=-1) -> int:
+    """Per-axis (m_n, r_n) plan (include/wino.h wino_plan_create_nd)."""
+    h = ctypes.c_void_p()
+    pad = (ctypes.c_int * N)(*([0] * N if padding is None else [int(p) for p in padding]))
+    mv = (ctypes.c_int * N)(*[int(v) for v in m])
+    rv = (ctypes.c_int * N)(*[int(v) for v in r])
+    _check(lib().wino_plan_create_nd(ctypes.byref(h), int(N), _i64arr(dims), mv, rv, int(C), int(K), int(batch),
+                                     pad, int(gemm_mode), int(device)))
     return h.value
 
 
@@ -260,6 +273,10 @@ class Plan:
     """One N-D Winograd conv layer F(m^N, r^N) on one GPU.
 
     Plan(N, dims, m, r, C, K, batch, padding=None, points=None, gemm_mode=0, fuse=0, device=-1)
+
+    m and r may be per-axis sequences (F(m_1 x .. x m_N, r_1 x .. x r_N),
+    wino_plan_create_nd); then g is [K][C][r_1]..[r_N] and points / fuse
+    must be left at their defaults.
     """
 
     def __init__(self, N: int, dims: Sequence[int], m: int, r: int, C: int, K: int, batch: int,
@@ -267,7 +284,17 @@ class Plan:
                  gemm_mode: int = WINO_GEMM_AUTO, fuse: int = 0, device: int = -1):
         self.N, self.dims, self.m, self.r, self.C, self.K, self.batch = N, tuple(dims), m, r, C, K, batch
         self.padding = tuple(padding) if padding is not None else (0,) * N
-        self.h = wino_plan_create_ex(N, dims, m, r, C, K, batch, self.padding, points, gemm_mode, fuse, device)
+        if isinstance(m, (list, tuple)) or isinstance(r, (list, tuple)):
+            mv = tuple(m) if isinstance(m, (list, tuple)) else (m,) * N
+            rv = tuple(r) if isinstance(r, (list, tuple)) else (r,) * N
+            if len(mv) != N or len(rv) != N:
+                raise ValueError("per-axis m and r need N entries")
+            if points is not None or fuse:
+                raise ValueError("per-axis plans take the default points and no fusion")
+            self.m, self.r = mv, rv
+            self.h = wino_plan_create_nd(N, dims, mv, rv, C, K, batch, self.padding, gemm_mode, device)
+        else:
+            self.h = wino_plan_create_ex(N, dims, m, r, C, K, batch, self.padding, points, gemm_mode, fuse, device)
         self.out_dims = wino_plan_out_dims(self.h, N)
         self.info = wino_plan_info(self.h)
 

@@ -1,0 +1,106 @@
+"""GPU parity for per-axis transforms F(m_1 x .. x m_N, r_1 x .. x r_N)
+(Eq. (4) indexes B_n, A_n, C_n by axis):
+wino_plan_create_nd against the float64 direct oracle on ragged shapes with
+padding, both GEMM schemes; e.g. F(2,3) along time with F(4,3) along space
+(the C3D-style video layer), anisotropic kernels such as 2x3 and 1x3.
+
+Tolerance (reading #17): relL2 <= 4e-7 * prod_n c_{alpha_n}, the
+per-axis product of reading #15's growth factors (c_1 = c_2 = 1, c_3 = 1.2,
+c_4 = 1.5, c_5 = 2.5, c_6 = 2.2, c_8 = 5); max-abs <= 10x that of max|y|.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1611_06565_b200 as pkg
+from oracle import direct
+
+pytestmark = pytest.mark.gpu
+
+GROWTH = {1: 1.0, 2: 1.0, 3: 1.2, 4: 1.5, 5: 2.5, 6: 2.2, 7: 3.5, 8: 5.0}
+
+CASES = [
+    # N, dims, m per axis, r per axis, pad, B, C, K
+    (3, (8, 14, 13), (2, 4, 4), (3, 3, 3), (1, 1, 1), 2, 16, 24),   # time F(2,3) x space F(4,3)
+    (3, (7, 9, 10), (4, 2, 2), (3, 3, 3), (1, 1, 1), 2, 8, 12),
+    (2, (17, 13), (4, 2), (3, 3), (1, 1), 3, 12, 20),
+    (2, (15, 19), (3, 2), (2, 3), (0, 1), 2, 10, 9),                  # anisotropic 2x3 kernel
+    (2, (9, 23), (2, 4), (1, 3), (0, 1), 2, 8, 8),                    # 1x3 kernel
+    (3, (6, 11, 12), (1, 4, 4), (1, 3, 3), (0, 1, 1), 2, 8, 16),      # 1x3x3 (2-D kernels in a 3-D net)
+    (4, (4, 5, 6, 7), (2, 2, 3, 2), (3, 2, 2, 3), (1, 0, 0, 1), 2, 4, 6),
+    (1, (40,), (5,), (4,), (2,), 2, 6, 7),                            # N = 1 (uniform: fused path)
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _inputs(dims, r, B, C, K, seed=0):
+    gen = torch.Generator("cpu").manual_seed(seed)
+    x = torch.randn((B, C) + tuple(dims), generator=gen)
+    g = torch.randn((K, C) + tuple(r), generator=gen) * math.sqrt(2.0 / (C * math.prod(r)))
+    return x.contiguous(), g.contiguous()
+
+
+def _tol(m, r):
+    return 4e-7 * math.prod(GROWTH[a + b - 1] for a, b in zip(m, r))
+
+
+@pytest.mark.parametrize("gemm_mode", [0, 1])
+@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", CASES)
+def test_per_axis_parity(N, dims, m, r, pad, B, C, K, gemm_mode):
+    x, g = _inputs(dims, r, B, C, K)
+    plan = pkg.Plan(N, dims, list(m), list(r), C, K, B, pad, gemm_mode=gemm_mode)
+    assert plan.info["n_points"] == math.prod(a + b - 1 for a, b in zip(m, r))
+    plan.filter_transform(g.cuda())
+    y = plan.forward(x.cuda()).cpu().double().numpy()
+    plan.close()
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), pad)
+    assert y.shape == ref.shape
+    rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    mx = np.abs(y - ref).max() / np.abs(ref).max()
+    tol = _tol(m, r)
+    print("m=%s r=%s mode=%d relL2=%.2e max=%.2e tol=%.1e" % (m, r, gemm_mode, rel, mx, tol))
+    assert rel <= tol and mx <= 10 * tol
+
+
+def test_per_axis_bias_relu_and_host_path():
+    N, dims, m, r, pad, B, C, K = CASES[0]
+    x, g = _inputs(dims, r, B, C, K, seed=3)
+    bias = torch.randn(K, generator=torch.Generator().manual_seed(9))
+    plan = pkg.Plan(N, dims, list(m), list(r), C, K, B, pad)
+    plan.filter_transform(g.cuda())
+    y = plan.forward(x.cuda()).cpu()
+    yb = plan.forward(x.cuda(), bias=bias.cuda(), relu=True).cpu()
+    # Eq. (2) epilogue: f(b + conv), in the spatial domain after A^T
+    assert torch.equal(yb, torch.clamp_min(y + bias.view(1, K, 1, 1, 1), 0.0))
+    # host-buffer entry point = device entry point, bit for bit
+    yh = torch.empty_like(y).pin_memory()
+    plan.forward_host(x.pin_memory(), yh)
+    assert torch.equal(yh, y)
+    plan.close()
+
+
+def test_equal_axes_take_the_fused_plan():
+    # per-axis entry point with equal (m_n, r_n): the single-(m, r) plan, same bits
+    x, g = _inputs((13, 11), (3, 3), 2, 8, 8)
+    p1 = pkg.Plan(2, (13, 11), [4, 4], [3, 3], 8, 8, 2, (1, 1))
+    p2 = pkg.Plan(2, (13, 11), 4, 3, 8, 8, 2, (1, 1))
+    for p in (p1, p2):
+        p.filter_transform(g.cuda())
+    assert torch.equal(p1.forward(x.cuda()), p2.forward(x.cuda()))
+    p1.close()
+    p2.close()
+
+
+def test_per_axis_errors():
+    with pytest.raises(pkg.WinoError):                 # alpha_0 = 9 > 8
+        pkg.Plan(2, (16, 16), [6, 2], [4, 3], 4, 4, 1, (1, 1))
+    with pytest.raises(ValueError):                    # points / fusion not per axis
+        pkg.Plan(2, (16, 16), [2, 4], [3, 3], 4, 4, 1, (1, 1), fuse=4)

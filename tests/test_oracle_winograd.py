@@ -107,3 +107,50 @@ def test_float64_winograd_vs_c_oracle(N, S, pts, pad, spatial):
     ref = direct.direct_conv_f64(x, g, pad)
     rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
     assert rel < 1e-12
+
+
+# per-axis transforms F(S_1 x .. x S_N, G_1 x .. x G_N) (Eq. (4) indexes B_n,
+# C_n, A_n by axis): exact equality with the brute-force sum
+PER_AXIS = [
+    # N, S per axis, G per axis, pad, spatial, B, C, K
+    (2, (2, 4), (3, 3), (1, 1), (5, 7), 1, 2, 2),       # F(2,3) x F(4,3)
+    (2, (4, 2), (3, 3), (0, 1), (7, 4), 2, 1, 2),
+    (2, (3, 2), (2, 3), (1, 0), (5, 6), 1, 2, 1),       # anisotropic kernel 2x3
+    (2, (2, 3), (1, 3), (0, 1), (3, 5), 1, 2, 2),       # r = (1, 3): D_0 = 2, trivial kernel axis
+    (3, (2, 4, 4), (3, 3, 3), (1, 1, 1), (3, 5, 4), 1, 2, 2),   # time F(2,3) x space F(4,3)
+    (3, (1, 2, 3), (3, 2, 3), (1, 0, 1), (3, 3, 4), 1, 1, 2),
+    (4, (2, 2, 3, 2), (3, 2, 2, 3), (1, 0, 0, 1), (2, 2, 3, 2), 1, 1, 1),
+]
+
+
+def _default_pts(S, G):
+    seq = ["0", "1", "-1", "2", "-2", "1/2", "-1/2", "3", "-3"]
+    D = S + G - 1
+    return ",".join(seq[:D - 1] + ["inf"]) if D > 1 else "0"
+
+
+@pytest.mark.parametrize("N,S,G,pad,spatial,B,C,K", PER_AXIS)
+def test_per_axis_exact_equals_direct(N, S, G, pad, spatial, B, C, K):
+    rng = random.Random(hash((N, S, G, pad)) & 0xffff)
+    mats = [tc.synthesize(S[n], G[n], _default_pts(S[n], G[n])) for n in range(N)]
+    A_, B_, C_ = ([m[i] for m in mats] for i in range(3))
+    x = _rand_frac(rng, (B, C) + spatial)
+    g = _rand_frac(rng, (K, C) + tuple(G))
+    y, st = wg.winograd_nd(x, g, pad, A_, B_, C_, exact=True)
+    ref = direct.direct_conv_py(x, g, pad)
+    assert y.shape == ref.shape
+    assert all(a == b for a, b in zip(y.ravel(), ref.ravel()))
+    # P = prod D_n transform points, T = B prod ceil(out_n / S_n) tiles
+    D = [S[n] + G[n] - 1 for n in range(N)]
+    assert st["U"].shape == (int(np.prod(D)), C, K)
+    assert st["V"].shape[1] == B * int(np.prod(st["tiles"]))
+
+
+def test_per_axis_equal_axes_is_the_single_transform():
+    rng = random.Random(7)
+    A_, B_, C_ = tc.synthesize(2, 3, "0,1,-1,inf")
+    x = _rand_frac(rng, (1, 2, 5, 4))
+    g = _rand_frac(rng, (2, 2, 3, 3))
+    y1, _ = wg.winograd_nd(x, g, (1, 1), A_, B_, C_, exact=True)
+    y2, _ = wg.winograd_nd(x, g, (1, 1), [A_, A_], [B_, B_], [C_, C_], exact=True)
+    assert all(a == b for a, b in zip(y1.ravel(), y2.ravel()))
