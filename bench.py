@@ -382,7 +382,10 @@ def run_nd(args, local):
                      "n_points": plan.info["n_points"],
                      "stages_ms": {s: round(v / calls, 4) for s, v in
                                    zip(["input_xform", "gemm", "output_xform"], stage_ms)},
-                     "path": "generic multi-pass per-axis transforms (xform_nd.cu) + tcgen05 3xTF32 GEMM"}
+                     "path": {0: "single F(m, r) fused kernels",
+                              1: "fused kernels with a distinct axis-0 transform (xform_mixed.cu)",
+                              2: "generic multi-pass per-axis transforms (xform_nd.cu)"}[plan.info["axis_mode"]]
+                             + " + tcgen05 3xTF32 GEMM"}
         plan.close()
         del xd, y
         torch.cuda.empty_cache()

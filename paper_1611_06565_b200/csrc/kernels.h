@@ -10,7 +10,8 @@ namespace wino {
 enum { kSpecRuntime = 0, kSpecDefault = 1, kSpecSeq = 2 };
 
 bool xform_supported(int N, int alpha, int m, int spec);
-bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma);
+// alpha0 / m0: axis 0's F(m0, r0) (= alpha / m except in per-axis plans)
+bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool tma);
 void plan_input_planes(KGeom& g, int64_t nwork, int num_sms);
 // a2: x [B][C][in...] -> V [P][C][T_s], input slabs [g.s_beg, g.s_beg + nslab)
 // (slab = b * nbox0 + box; V row = t - g.t0)
@@ -28,6 +29,12 @@ cudaError_t launch_input_nd(const float* x, float* V, const KGeom& g, const NdPa
                             int64_t t_lo, int64_t t_hi, cudaStream_t s);
 cudaError_t launch_output_nd(const float* Mx, float* W, float* y, const KGeom& g, const NdParams& q, int N,
                              int64_t t_lo, int64_t t_hi, cudaStream_t s);
+// per-axis plans with a distinct axis 0 and fused kernels (xform_mixed.cu)
+bool mixed_supported(int N, int alpha0, int m0, int alpha, int m);
+cudaError_t launch_input_mixed(int N, int alpha0, int m0, int alpha, int m, const float* x, float* V, const KGeom& g,
+                               const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
+cudaError_t launch_output_mixed(int N, int alpha0, int m0, int alpha, int m, const float* Mx, float* y,
+                                const KGeom& g, const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s);
 

@@ -201,6 +201,9 @@ struct wino_plan_s {
   // per-axis (m_n, r_n) plan (wino_plan_create_nd with unequal axes):
   // generic multi-pass transforms (xform_nd.cu), scratch W for the output passes
   bool nd = false;
+  // fused plan with a distinct axis 0 (F(m0, r0); xform_mixed.cu)
+  bool mixed = false;
+  int m0 = 0, r0 = 0, a0 = 0;
   int mn[kMaxN]{}, rn[kMaxN]{}, an[kMaxN]{};
   NdParams ndp{};
   float* W = nullptr;
@@ -240,9 +243,12 @@ wino_status wino_synthesize(int m, int r, const char* points, double* AT, double
   return WINO_OK;
 }
 
-wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dims, int m, int r, int C, int K,
-                                int batch, const int* padding, const char* points, int gemm_mode, int fuse,
-                                int device) {
+// The fused-kernel plan: F(m, r) on axes 1..N-1 and F(m0, r0) on axis 0
+// (m0 = m, r0 = r for single-(m, r) plans; a distinct axis 0 only for the
+// instantiated per-axis combinations, mixed_supported()).
+static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims, int m0, int r0, int m, int r, int C,
+                               int K, int batch, const int* padding, const char* points, int gemm_mode, int fuse,
+                               int device) {
   if (!plan_out) return fail(WINO_ERR_ARG, "plan pointer is NULL");
   *plan_out = nullptr;
   if (N < 1 || N > kMaxN) return fail(WINO_ERR_ARG, "N must be in 1..4 (got %d)", N);
@@ -250,16 +256,28 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
   if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
   if (fuse & ~WINO_FUSE_L2_CHUNK) return fail(WINO_ERR_UNSUPPORTED, "fuse bitmask %d not implemented in this build", fuse);
-  Transforms t;
-  int spec;
+  Transforms t, t0;
+  int spec, spec0;
   wino_status st = synth_checked(m, r, points, t, spec);
   if (st) return st;
-  const int a = t.a;
-  if (a > kMaxA || !xform_supported(N, a, m, spec))
+  const bool mixed = m0 != m || r0 != r;
+  if (mixed) {
+    st = synth_checked(m0, r0, nullptr, t0, spec0);
+    if (st) return st;
+  } else {
+    t0 = t;
+    spec0 = spec;
+  }
+  const int a = t.a, a0 = t0.a;
+  if (mixed && (spec == kSpecRuntime || spec0 == kSpecRuntime || points || fuse || !mixed_supported(N, a0, m0, a, m)))
+    return fail(WINO_ERR_UNSUPPORTED, "no fused kernels for axis-0 F(%d,%d) with F(%d,%d) on N=%d", m0, r0, m, r, N);
+  if (a > kMaxA || a0 > kMaxA || (!mixed && !xform_supported(N, a, m, spec)))
     return fail(WINO_ERR_UNSUPPORTED, "no device transform kernels for N=%d alpha=%d m=%d", N, a, m);
 
   wino_plan_s* p = new wino_plan_s();
   p->N = N; p->m = m; p->r = r; p->a = a; p->C = C; p->K = K; p->batch = batch;
+  p->mixed = mixed;
+  p->m0 = m0; p->r0 = r0; p->a0 = a0;
   p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? WINO_GEMM_3XTF32 : gemm_mode;
   p->fuse = fuse;
   p->spec = spec;
@@ -270,29 +288,30 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
     p->in[n] = dims[n];
     p->pad[n] = padding ? padding[n] : 0;
     if (dims[n] < 1 || p->pad[n] < 0) { delete p; return fail(WINO_ERR_ARG, "dims must be >= 1 and padding >= 0"); }
-    p->out[n] = dims[n] + 2 * p->pad[n] - r + 1;
-    if (p->out[n] < 1) { delete p; return fail(WINO_ERR_SHAPE, "kernel %d larger than padded input %lld on axis %d", r, (long long)(dims[n] + 2 * p->pad[n]), n); }
-    p->tiles[n] = (int)((p->out[n] + m - 1) / m);
+    const int rn = n == 0 ? r0 : r, mn = n == 0 ? m0 : m;
+    p->out[n] = dims[n] + 2 * p->pad[n] - rn + 1;
+    if (p->out[n] < 1) { delete p; return fail(WINO_ERR_SHAPE, "kernel %d larger than padded input %lld on axis %d", rn, (long long)(dims[n] + 2 * p->pad[n]), n); }
+    p->tiles[n] = (int)((p->out[n] + mn - 1) / mn);
     Tps *= p->tiles[n];
   }
   p->Tps = Tps;
   const int64_t T = Tps * batch;
   if (T > (int64_t)INT32_MAX - 256) { delete p; return fail(WINO_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)T); }
   p->T_s = (T + 127) / 128 * 128;
-  p->P = ipow(a, N);
+  p->P = (int64_t)a0 * ipow(a, N - 1);
   const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32;
   const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
   p->K_s = tc ? (K + bn - 1) / bn * bn : (K + 31) / 32 * 32;
 
   // tables
-  const FloatTables ft = to_tables(t);
+  const FloatTables ft = to_tables(t), ft0 = to_tables(t0);
   for (int i = 0; i < kMaxA; ++i)
     for (int j = 0; j < kMaxA; ++j) {
       p->xp.AT[i][j] = ft.AT[i][j];
       p->xp.BT[i][j] = ft.BT[i][j];
-      for (int n = 0; n < kMaxN; ++n) p->fp.G[n][i][j] = ft.G[i][j];
+      for (int n = 0; n < kMaxN; ++n) p->fp.G[n][i][j] = n == 0 ? ft0.G[i][j] : ft.G[i][j];
     }
-  for (int n = 0; n < kMaxN; ++n) { p->fp.a[n] = a; p->fp.r[n] = r; }
+  for (int n = 0; n < kMaxN; ++n) { p->fp.a[n] = n == 0 ? a0 : a; p->fp.r[n] = n == 0 ? r0 : r; }
   p->fp.N = N; p->fp.C = C; p->fp.K = K; p->fp.K_s = (int)p->K_s; p->fp.P = p->P;
 
   KGeom& g = p->geom;
@@ -306,7 +325,7 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   // the TMA slab needs 16-byte strides and the compile-time tables
   const bool tma_shape = N >= 2 && spec != kSpecRuntime && (p->in[N - 1] % 4) == 0;
   p->use_tma_in = p->use_tma_in && tma_shape;
-  if (!plan_input_slab(g, N, a, m, p->use_tma_in)) {
+  if (!plan_input_slab(g, N, a0, m0, a, m, p->use_tma_in)) {
     delete p;
     return fail(WINO_ERR_UNSUPPORTED, "input slab of one axis-0 tile exceeds shared memory (inner extents too large)");
   }
@@ -389,6 +408,12 @@ wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dim
   return WINO_OK;
 }
 
+wino_status wino_plan_create_ex(wino_plan_t* plan_out, int N, const int64_t* dims, int m, int r, int C, int K,
+                                int batch, const int* padding, const char* points, int gemm_mode, int fuse,
+                                int device) {
+  return create_core(plan_out, N, dims, m, r, m, r, C, K, batch, padding, points, gemm_mode, fuse, device);
+}
+
 wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
                                 int C, int K, int batch, const int* padding, int gemm_mode, int device) {
   if (!plan_out) return fail(WINO_ERR_ARG, "plan pointer is NULL");
@@ -402,6 +427,15 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   // equal axes: the single-(m, r) plan and its fused kernels
   if (uniform) return wino_plan_create_ex(plan_out, N, dims, m[0], r[0], C, K, batch, padding, nullptr, gemm_mode, 0,
                                           device);
+  // a distinct axis 0 over equal other axes with instantiated fused kernels
+  // (e.g. F(2,3) along time x F(4,3) along space); WINO_ND_GENERIC=1 forces
+  // the generic multi-pass path (dev / test knob)
+  bool rest_equal = N >= 2;
+  for (int n = 2; n < N; ++n) rest_equal = rest_equal && m[n] == m[1] && r[n] == r[1];
+  const char* ev_gen = getenv("WINO_ND_GENERIC");
+  if (rest_equal && !(ev_gen && atoi(ev_gen) != 0) && m[0] + r[0] - 1 <= kMaxA && m[1] + r[1] - 1 <= kMaxA &&
+      mixed_supported(N, m[0] + r[0] - 1, m[0], m[1] + r[1] - 1, m[1]) && r[0] == 3 && r[1] == 3)
+    return create_core(plan_out, N, dims, m[0], r[0], m[1], r[1], C, K, batch, padding, nullptr, gemm_mode, 0, device);
   Transforms tn[kMaxN];
   int64_t P = 1;
   for (int n = 0; n < N; ++n) {
@@ -616,7 +650,11 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     g.T = t_hi;
     ProfScope ps{p, s, 0};
     if (rec) CUDA_TRY(ps.begin());
-    CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, tm, (int)(s1 - s0), s));
+    if (p->mixed) {
+      CUDA_TRY(launch_input_mixed(p->N, p->a0, p->m0, p->a, p->m, x, p->V, g, p->xp, tm, (int)(s1 - s0), s));
+    } else {
+      CUDA_TRY(launch_input_xform(p->N, p->a, p->m, p->spec, x, p->V, g, p->xp, tm, (int)(s1 - s0), s));
+    }
     if (rec) CUDA_TRY(ps.end());
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
@@ -628,7 +666,12 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(pg.end());
     ProfScope po{p, s, 2};
     if (rec) CUDA_TRY(po.begin());
-    CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, p->tm_M_ok ? &p->tm_M : nullptr, s));
+    if (p->mixed) {
+      CUDA_TRY(launch_output_mixed(p->N, p->a0, p->m0, p->a, p->m, p->M, y, g, p->xp,
+                                   p->tm_M_ok ? &p->tm_M : nullptr, s));
+    } else {
+      CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, p->tm_M_ok ? &p->tm_M : nullptr, s));
+    }
     if (rec) CUDA_TRY(po.end());
   }
   if (rec) ++p->prof_calls;
@@ -718,10 +761,10 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
-  const int64_t v[19] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[20] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
-                         p->geom.npl};
+                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

@@ -13,8 +13,9 @@ namespace wino {
 // memory.  With `tma` the last-axis rows start dL = (-P_last) mod 4 columns
 // early (16-byte aligned TMA start).  Returns false if even a one-tile-deep
 // slab exceeds 200 KB.
-bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
-  const int halo = alpha - m;
+bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool tma) {
+  const int halo = alpha - m;      // axes >= 1
+  const int halo0 = alpha0 - m0;   // axis 0 (its own F(m0, r0) in per-axis plans)
   const int pl = g.pad[N - 1];
   g.dL = (tma && N >= 2) ? ((4 - pl % 4) % 4) : 0;
   int inner = 1;  // floats of one axis-0 slab slice
@@ -36,11 +37,11 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
   const bool hmode = N == 3 && alpha >= 6;
   g.hpitch = hmode ? (g.e[2] + 3) / 4 * 4 : 0;
   auto slab = [&](int bt) {
-    const int e0 = bt * m + halo;
+    const int e0 = bt * m0 + halo0;
     if (N == 1) return (size_t)((e0 + 3) / 4 * 4) * 4;
     return (size_t)e0 * inner * 4;
   };
-  auto hbytes = [&](int bt) { return hmode ? (size_t)bt * alpha * g.e[1] * g.hpitch * 4 : (size_t)0; };
+  auto hbytes = [&](int bt) { return hmode ? (size_t)bt * alpha0 * g.e[1] * g.hpitch * 4 : (size_t)0; };
   // one slab (+ H) near 64 KB (48 KB in H mode: measured c4 337 -> 288 us at bt0 = 1)
   int bt0 = g.tiles[0];
   size_t target = hmode ? 48 * 1024 : 64 * 1024;
@@ -56,7 +57,7 @@ bool plan_input_slab(KGeom& g, int N, int alpha, int m, bool tma) {
   g.bt0 = bt0;
   g.npl = 1;  // plan_input_planes() raises it
   g.nbox0 = (g.tiles[0] + bt0 - 1) / bt0;
-  g.e[0] = bt0 * m + halo;
+  g.e[0] = bt0 * m0 + halo0;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
   g.in_threads = 256;
   if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256)

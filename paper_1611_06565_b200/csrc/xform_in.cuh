@@ -65,12 +65,24 @@ __device__ __forceinline__ void load_row(const float* p, float* r) {
   load_seg<cap, D, D + A>(p, r);
 }
 
+// Axis-0 transform of a plan: F(M0, .) with alpha_0 = A0 and table Tab0.
+// Equal to the other axes' (A, M, Tab) for the usual single-(m, r) plans; a
+// different one for the per-axis plans with a distinct axis 0 (e.g. F(2,3)
+// along time and F(4,3) along space, NEXT-2, Eq. (4)).
+template <int A0_, int M0_, class Tab0_>
+struct Ax0 {
+  static constexpr int A = A0_;
+  static constexpr int M = M0_;
+  using Tab = Tab0_;
+};
+
 // One work item: axis-0 output point X0 of one tile whose window starts at
 // slab offset `base` (+ D columns); writes alpha^(N-1) values of V.
-template <int N, int A, int M, class Tab, int D, int X0>
+template <int N, int A, int M, class Tab, int D, int X0, class Ax>
 __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, const KGeom& g,
                                         const XfParams& xp, float* __restrict__ vout, int64_t pstride) {
   using Get = BTget<Tab>;
+  using Get0 = BTget<typename Ax::Tab>;
   if constexpr (N == 1) {
     float h[A];
     load_row<A, M, D>(S + base, h);
@@ -78,6 +90,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
 #pragma unroll
     for (int j = 0; j < A; ++j) vout[j * pstride] = h[j];
   } else if constexpr (N == 2) {
+    static_assert(Ax::A == A && Ax::M == M, "N = 2 whole-tile items need equal axes");
     // the whole alpha x alpha window in registers: every window row is read
     // once (no per-xi_0 re-reads), both axes transformed in place
     float h[A * A];
@@ -95,9 +108,9 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     for (int j = 0; j < P1; ++j) h[j] = 0.f;
     bool first = true;
 #pragma unroll
-    for (int i0 = 0; i0 < A; ++i0) {
-      if (!Get::nz(xp, X0, i0)) continue;
-      const float bv = Get::v(xp, X0, i0);
+    for (int i0 = 0; i0 < Ax::A; ++i0) {
+      if (!Get0::nz(xp, X0, i0)) continue;
+      const float bv = Get0::v(xp, X0, i0);
 #pragma unroll
       for (int rw = 0; rw < ROWS; ++rw) {
         int off = base + i0 * g.sst[0];
@@ -117,12 +130,12 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
   }
 }
 
-template <int N, int A, int M, class Tab, int D, int X0 = 0>
+template <int N, int A, int M, class Tab, int D, class Ax, int X0 = 0>
 __device__ __forceinline__ void in_dispatch(int xi0, const float* S, int base, const KGeom& g, const XfParams& xp,
                                             float* vout, int64_t pstride) {
-  if constexpr (X0 < A) {
-    if (xi0 == X0) in_work<N, A, M, Tab, D, X0>(S, base, g, xp, vout, pstride);
-    else in_dispatch<N, A, M, Tab, D, X0 + 1>(xi0, S, base, g, xp, vout, pstride);
+  if constexpr (X0 < Ax::A) {
+    if (xi0 == X0) in_work<N, A, M, Tab, D, X0, Ax>(S, base, g, xp, vout, pstride);
+    else in_dispatch<N, A, M, Tab, D, Ax, X0 + 1>(xi0, S, base, g, xp, vout, pstride);
   }
 }
 
@@ -220,7 +233,7 @@ struct PlaneInfo {
 // of its tiles.  Work items of all planes form one pool, so every round of
 // the block keeps all warps busy and the V stores of neighbouring planes
 // (adjacent t) are issued together.
-template <int N, int A, int M, class Tab, int D>
+template <int N, int A, int M, class Tab, int D, class Ax>
 __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int slab_f, float* __restrict__ H,
                                                  float* __restrict__ V, const KGeom& g, const XfParams& xp,
                                                  const PlaneInfo* pl, int npl, uint32_t mb0) {
@@ -249,6 +262,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
   // ---- N = 3, alpha >= 6: the axis-0 pass materialised in shared memory
   if constexpr (N == 3 && A >= 6) {
     using Get = BTget<Tab>;
+    using Get0 = BTget<typename Ax::Tab>;   // axis 0: alpha_0 = Ax::A, step Ax::M
+    constexpr int A0 = Ax::A, M0 = Ax::M;
     const int e1 = g.e[1], e2 = g.e[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int tl1 = g.tiles[1], tl2 = g.tiles[2];
@@ -262,17 +277,17 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         float* row = S0 + p * slab_f + y * g.sst[1] + D;
         for (int xh = lane; xh < e2; xh += 32) {
           float* col = row + xh;
-          float v[A];
+          float v[A0];
 #pragma unroll
-          for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
+          for (int i = 0; i < A0; ++i) v[i] = col[i * g.sst[0]];
 #pragma unroll
-          for (int x0 = 0; x0 < A; ++x0) {
+          for (int x0 = 0; x0 < A0; ++x0) {
             float acc = 0.f;
             bool first = true;
 #pragma unroll
-            for (int i = 0; i < A; ++i) {
-              if (Get::nz(xp, x0, i)) {
-                acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
+            for (int i = 0; i < A0; ++i) {
+              if (Get0::nz(xp, x0, i)) {
+                acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
                 first = false;
               }
             }
@@ -286,7 +301,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // (npl planes are adjacent in t) into each of the alpha^2 planes of V
       // it touches (measured: the V store pattern bounds this kernel)
       const int R = tl1 * tl2, nrun = npl * R;
-      for (int u = threadIdx.x; u < A * nrun; u += blockDim.x) {
+      for (int u = threadIdx.x; u < A0 * nrun; u += blockDim.x) {
         const int xi0 = u / nrun;
         const int w = u - xi0 * nrun;
         const int p = w / R;
@@ -312,19 +327,19 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     for (int r = warp; r < nt0 * e1; r += nwarps) {
       const int y = r % e1, t0l = r / e1;
       for (int xh = lane; xh < e2; xh += 32) {
-        const float* col = S0 + t0l * M * g.sst[0] + y * g.sst[1] + xh + D;
-        float v[A];
+        const float* col = S0 + t0l * M0 * g.sst[0] + y * g.sst[1] + xh + D;
+        float v[A0];
 #pragma unroll
-        for (int i = 0; i < A; ++i) v[i] = col[i * g.sst[0]];
-        float* hrow = H + (t0l * A * e1 + y) * hp + xh;
+        for (int i = 0; i < A0; ++i) v[i] = col[i * g.sst[0]];
+        float* hrow = H + (t0l * A0 * e1 + y) * hp + xh;
 #pragma unroll
-        for (int x0 = 0; x0 < A; ++x0) {
+        for (int x0 = 0; x0 < A0; ++x0) {
           float acc = 0.f;
           bool first = true;
 #pragma unroll
-          for (int i = 0; i < A; ++i) {
-            if (Get::nz(xp, x0, i)) {
-              acc = first ? Get::v(xp, x0, i) * v[i] : fmaf(Get::v(xp, x0, i), v[i], acc);
+          for (int i = 0; i < A0; ++i) {
+            if (Get0::nz(xp, x0, i)) {
+              acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
               first = false;
             }
           }
@@ -336,13 +351,13 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     // phase 2: one work item per (t0, xi_0, t1, t2): the alpha x alpha window
     // of plane (t0, xi_0) in registers, axes 1 and 2 transformed in place
     float* __restrict__ vb = vbase(0);
-    for (int w = threadIdx.x; w < nt0 * A * tl1 * tl2; w += blockDim.x) {
+    for (int w = threadIdx.x; w < nt0 * A0 * tl1 * tl2; w += blockDim.x) {
       const int t2 = w % tl2;
       int r = w / tl2;
       const int t1 = r % tl1;
       r /= tl1;
-      const int xi0 = r % A, t0l = r / A;
-      const float* hp0 = H + ((t0l * A + xi0) * e1 + t1 * M) * hp + t2 * M;
+      const int xi0 = r % A0, t0l = r / A0;
+      const float* hp0 = H + ((t0l * A0 + xi0) * e1 + t1 * M) * hp + t2 * M;
       float h[A * A];
 #pragma unroll
       for (int i1 = 0; i1 < A; ++i1) load_row<A, M, 0>(hp0 + i1 * hp, h + i1 * A);
@@ -353,7 +368,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     }
   } else {
     // ---- work items (plane, xi_0, tile), tile fastest
-    constexpr int NX = N >= 3 ? A : 1;        // work items per tile (one per xi_0 when N >= 3)
+    constexpr int NX = N >= 3 ? Ax::A : 1;    // work items per tile (one per xi_0 when N >= 3)
     if (npl == 1) {
       // one plane: no plane index to decode (the common case for large slabs)
       ensure(0);
@@ -369,8 +384,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           rem /= g.tiles[ax];
           base += ti * M * g.sst[ax];
         }
-        base += rem * M * g.sst[0];
-        in_dispatch<N, A, M, Tab, D>(xi0, S0, base, g, xp, vb + tl, pstride);
+        base += rem * Ax::M * g.sst[0];
+        in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride);
       }
       return;
     }
@@ -391,8 +406,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         rem /= g.tiles[ax];
         base += ti * M * g.sst[ax];
       }
-      base += rem * M * g.sst[0];
-      in_dispatch<N, A, M, Tab, D>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride);
+      base += rem * Ax::M * g.sst[0];
+      in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride);
     }
   }
 }
@@ -402,7 +417,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
 // the same channel).  kTma (N >= 2): each slab is one TMA box starting D
 // columns left of -P_last, all npl boxes issued at once; !kTma: cp.async
 // fallback, D == 0.
-template <int N, int A, int M, class Tab, int D, bool kTma>
+template <int N, int A, int M, class Tab, int D, bool kTma, class Ax = Ax0<A, M, Tab>>
 __global__ void __launch_bounds__(256)
 k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
               const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm, int nslab) {
@@ -435,7 +450,7 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int p = 0; p < npl; ++p) {
         const PlaneInfo q = plane(w0 + p);
-        issue_slab_tma<N, M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, mb0 + 8u * p);
+        issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, mb0 + 8u * p);
       }
     }
     __syncthreads();
@@ -443,10 +458,10 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
     static_assert(D == 0, "the cp.async slab path is unshifted");
     __syncthreads();
     for (int p = 0; p < npl; ++p)
-      load_slab_cpasync<N, A, M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c);
+      load_slab_cpasync<N, Ax::A, Ax::M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c);
     __syncthreads();
   }
-  transform_planes<N, A, M, Tab, D>(smem_f, slab_f, H, V, g, xp, pl, npl,
+  transform_planes<N, A, M, Tab, D, Ax>(smem_f, slab_f, H, V, g, xp, pl, npl,
                                     kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u);
 }
 
@@ -470,16 +485,16 @@ inline cudaError_t launch_in_kern(K kern, const float* x, float* V, const KGeom&
 // Launch one (N, alpha, m, table) instantiation over slabs [g.s_beg,
 // g.s_beg + nslab).  tm != NULL selects the TMA slab (g.dL is its column
 // shift, 0 or 3); kAllowTma = false compiles only the fallback (run-time tables).
-template <int N, int A, int M, class Tab, bool kAllowTma>
+template <int N, int A, int M, class Tab, bool kAllowTma, class Ax = Ax0<A, M, Tab>>
 cudaError_t launch_in(const float* x, float* V, const KGeom& g, const XfParams& xp, const CUtensorMap* tm, int nslab,
                       cudaStream_t s) {
   if constexpr (kAllowTma && N >= 2) {
-    if (tm && g.dL == 0) return launch_in_kern(k_input_xform<N, A, M, Tab, 0, true>, x, V, g, xp, *tm, nslab, s);
-    if (tm && g.dL == 3) return launch_in_kern(k_input_xform<N, A, M, Tab, 3, true>, x, V, g, xp, *tm, nslab, s);
+    if (tm && g.dL == 0) return launch_in_kern(k_input_xform<N, A, M, Tab, 0, true, Ax>, x, V, g, xp, *tm, nslab, s);
+    if (tm && g.dL == 3) return launch_in_kern(k_input_xform<N, A, M, Tab, 3, true, Ax>, x, V, g, xp, *tm, nslab, s);
   }
   KGeom g1 = g;
   CUtensorMap dummy{};
-  return launch_in_kern(k_input_xform<N, A, M, Tab, 0, false>, x, V, g1, xp, dummy, nslab, s);
+  return launch_in_kern(k_input_xform<N, A, M, Tab, 0, false, Ax>, x, V, g1, xp, dummy, nslab, s);
 }
 
 template <int A, int M, class Tab, bool kAllowTma>

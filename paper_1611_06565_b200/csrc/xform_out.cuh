@@ -15,29 +15,39 @@ namespace out_detail {
 // One thread per (tile t, output channel k): read M[xi][k][t] for all xi,
 // apply A^T along every axis (alpha -> m), crop to `out` and scatter into y.
 
+// Axis-0 transform of a plan (alpha_0 = A, tile step M, table Tab); equal to
+// the other axes' except for per-axis plans with a distinct axis 0 (NEXT-2).
+template <int A0_, int M0_, class Tab0_>
+struct OAx0 {
+  static constexpr int A = A0_;
+  static constexpr int M = M0_;
+  using Tab = Tab0_;
+};
+
 // Accumulate axis-0 group x1 (the alpha^(N-1) values v of M[xi][k][t] with
-// xi_0 = x1) into the output tile o: A^T along axes 1..N-1 in registers,
-// then o += A^T[:, x1] (x) v along axis 0.
-template <int N, int A, int M, class Tab>
-__device__ __forceinline__ void accum_group(float (&o)[ipow(M, N)], float (&v)[ipow(A, N - 1)], int x1,
+// xi_0 = x1) into the output tile o (M_0 x M^(N-1)): A^T along axes 1..N-1
+// in registers, then o += A_0^T[:, x1] (x) v along axis 0.
+template <int N, int A, int M, class Tab, class Ax>
+__device__ __forceinline__ void accum_group(float (&o)[Ax::M * ipow(M, N - 1)], float (&v)[ipow(A, N - 1)], int x1,
                                             const XfParams& xp) {
   constexpr int M1 = ipow(M, N - 1);
+  using Get0 = ATget<typename Ax::Tab>;
   all_axes<A, N - 1, M, M, ATget<Tab>>(v, xp);
 #pragma unroll
-  for (int o1 = 0; o1 < M; ++o1) {
-    if (!ATget<Tab>::nz(xp, o1, x1)) continue;
-    const float av = ATget<Tab>::v(xp, o1, x1);
+  for (int o1 = 0; o1 < Ax::M; ++o1) {
+    if (!Get0::nz(xp, o1, x1)) continue;
+    const float av = Get0::v(xp, o1, x1);
 #pragma unroll
     for (int rr = 0; rr < M1; ++rr)
       o[o1 * M1 + rr] = fmaf(av, v[digits_to_base(rr, N - 1, M, A)], o[o1 * M1 + rr]);
   }
 }
 
-template <int N, int M>
-__device__ __forceinline__ void store_tile(float (&o)[ipow(M, N)], float* __restrict__ y, const KGeom& g, int64_t t,
-                                           int k) {
-  constexpr int M1 = ipow(M, N - 1);
-  constexpr int MN = ipow(M, N);
+template <int N, int M, int M0 = M>
+__device__ __forceinline__ void store_tile(float (&o)[M0 * ipow(M, N - 1)], float* __restrict__ y, const KGeom& g,
+                                           int64_t t, int k) {
+  constexpr int M1 = M0 * ipow(M, N - 2);   // output rows along the last axis (N >= 2)
+  constexpr int MN = M0 * ipow(M, N - 1);
   // Eq. (2) epilogue in the spatial domain: d' = f(b + conv)
   if (g.bias || g.act) {
     const float bk = g.bias ? __ldg(g.bias + k) : 0.f;
@@ -57,45 +67,47 @@ __device__ __forceinline__ void store_tile(float (&o)[ipow(M, N)], float* __rest
     rem /= g.tiles[n];
   }
   float* yb = y + ((int64_t)rem * g.K + k) * g.out_vol;
-  const int lastpos = gi[N - 1] * M;
-  const bool full_last = lastpos + M <= g.out[N - 1];
+  constexpr int ML = N == 1 ? M0 : M;  // tile length along the last axis
+  const int lastpos = gi[N - 1] * ML;
+  const bool full_last = lastpos + ML <= g.out[N - 1];
 #pragma unroll
-  for (int rr = 0; rr < M1; ++rr) {  // each output row along the last axis
+  for (int rr = 0; rr < (N == 1 ? 1 : M1); ++rr) {  // each output row along the last axis
     bool ok = true;
     int64_t off = lastpos;
 #pragma unroll
     for (int ax = 0; ax < N - 1; ++ax) {
-      const int d = (rr / ipow(M, N - 2 - ax)) % M;
-      const int pos = gi[ax] * M + d;
+      // row digits: axis 0 has radix M0, the others M
+      const int d = ax == 0 ? rr / ipow(M, N - 2) : (rr / ipow(M, N - 2 - ax)) % M;
+      const int pos = gi[ax] * (ax == 0 ? M0 : M) + d;
       ok = ok && (pos < (int)g.out[ax]);
       off += (int64_t)pos * g.out_stride[ax];
     }
     if (!ok) continue;
     float* dst = yb + off;
-    const int ob = rr * M;  // o index of (row, last = 0); last axis fastest
-    if constexpr (M == 4) {
+    const int ob = rr * ML;  // o index of (row, last = 0); last axis fastest
+    if constexpr (ML == 4) {
       if (full_last && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
         *reinterpret_cast<float4*>(dst) = make_float4(o[ob], o[ob + 1], o[ob + 2], o[ob + 3]);
         continue;
       }
-    } else if constexpr (M == 2) {
+    } else if constexpr (ML == 2) {
       if (full_last && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
         *reinterpret_cast<float2*>(dst) = make_float2(o[ob], o[ob + 1]);
         continue;
       }
     }
 #pragma unroll
-    for (int l = 0; l < M; ++l)
+    for (int l = 0; l < ML; ++l)
       if (lastpos + l < g.out[N - 1]) dst[l] = o[ob + l];
   }
 }
 
-template <int N, int A, int M, class Tab>
+template <int N, int A, int M, class Tab, class Ax = OAx0<A, M, Tab>>
 __global__ void __launch_bounds__(128)
 k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid_constant__ KGeom g,
                const __grid_constant__ XfParams xp) {
   constexpr int A1 = ipow(A, N - 1);
-  constexpr int MN = ipow(M, N);
+  constexpr int MN = Ax::M * ipow(M, N - 1);
   pdl_wait();      // M comes from the GEMM
   pdl_trigger();
   const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
@@ -109,16 +121,16 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
 #pragma unroll
   for (int j = 0; j < MN; ++j) o[j] = 0.f;
 #pragma unroll
-  for (int x1 = 0; x1 < A; ++x1) {
+  for (int x1 = 0; x1 < Ax::A; ++x1) {
     float v[A1];
 #pragma unroll
     for (int j = 0; j < A1; ++j) {
       v[j] = __ldg(src);
       src += pstride;
     }
-    accum_group<N, A, M, Tab>(o, v, x1, xp);
+    accum_group<N, A, M, Tab, Ax>(o, v, x1, xp);
   }
-  store_tile<N, M>(o, y, g, t, k);
+  store_tile<N, M, Ax::M>(o, y, g, t, k);
 }
 
 // TMA-fed variant (persistent): a CTA of 128 threads walks units (t-block of
@@ -128,12 +140,13 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
 // runs ns - 1 groups ahead (across unit boundaries); threads read their
 // column (conflict-free) and accumulate as above.  Keeps tens of KB of M in
 // flight per SM without the per-thread load latency of the plain kernel.
-template <int N, int A, int M, class Tab>
+template <int N, int A, int M, class Tab, class Ax = OAx0<A, M, Tab>>
 __global__ void __launch_bounds__(128)
 k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const __grid_constant__ XfParams xp,
                    const __grid_constant__ CUtensorMap tmM, int ns) {
   constexpr int A1 = ipow(A, N - 1);
-  constexpr int MN = ipow(M, N);
+  constexpr int MN = Ax::M * ipow(M, N - 1);
+  constexpr int A0 = Ax::A;
   constexpr uint32_t kStageBytes = A1 * 128 * 4;
   extern __shared__ __align__(128) float S[];
   __shared__ __align__(8) uint64_t full[kMaxOutStages];
@@ -141,9 +154,9 @@ k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const
   const int64_t nunits = (int64_t)nblk * g.K;
   const uint32_t fb0 = (uint32_t)__cvta_generic_to_shared(&full[0]);
   const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(S);
-  // group q of this CTA: its (q / A)-th unit, xi_0 = q % A
+  // group q of this CTA: its (q / A0)-th unit, xi_0 = q % A0
   auto issue = [&](int64_t q, int st) {
-    const int64_t u = blockIdx.x + (q / A) * gridDim.x;
+    const int64_t u = blockIdx.x + (q / A0) * gridDim.x;
     if (u >= nunits) return;
     const int k = (int)(u / nblk), tb = (int)(u - (int64_t)k * nblk);
     const int tc = (int)(g.t_beg - g.t0) + tb * 128;
@@ -151,7 +164,7 @@ k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStageBytes) : "memory");
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-        ::"r"(sb0 + st * kStageBytes), "l"(&tmM), "r"(tc), "r"(k), "r"((int)(q % A) * A1), "r"(bar)
+        ::"r"(sb0 + st * kStageBytes), "l"(&tmM), "r"(tc), "r"(k), "r"((int)(q % A0) * A1), "r"(bar)
         : "memory");
   };
   if (threadIdx.x == 0) {
@@ -171,7 +184,7 @@ k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const
 #pragma unroll
     for (int j = 0; j < MN; ++j) o[j] = 0.f;
 #pragma unroll
-    for (int x1 = 0; x1 < A; ++x1, ++q) {
+    for (int x1 = 0; x1 < A0; ++x1, ++q) {
       const int st = (int)(q % ns);
       const uint32_t par = (uint32_t)((q / ns) & 1);
       uint32_t done = 0;
@@ -188,9 +201,9 @@ k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const
       for (int j = 0; j < A1; ++j) v[j] = col[j * 128];
       __syncthreads();  // every thread has read stage st: refill it ns groups ahead
       if (threadIdx.x == 0) issue(q + ns, st);
-      accum_group<N, A, M, Tab>(o, v, x1, xp);
+      accum_group<N, A, M, Tab, Ax>(o, v, x1, xp);
     }
-    if (t < g.T) store_tile<N, M>(o, y, g, t, k);
+    if (t < g.T) store_tile<N, M, Ax::M>(o, y, g, t, k);
   }
 }
 
@@ -208,13 +221,13 @@ constexpr int out_stages() {
   return (A1 < 32 || A1 > 256) ? 0 : n >= kMaxOutStages ? kMaxOutStages : n >= 2 ? n : 0;
 }
 
-template <int N, int A, int M, class Tab>
+template <int N, int A, int M, class Tab, class Ax = OAx0<A, M, Tab>>
 cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams& xp, const CUtensorMap* tmM,
                        cudaStream_t s) {
   constexpr int ns = out_stages<N, A>();
   if constexpr (ns > 0) {
     if (tmM) {
-      auto kern = k_output_xform_tma<N, A, M, Tab>;
+      auto kern = k_output_xform_tma<N, A, M, Tab, Ax>;
       constexpr int smem = ns * ipow(A, N - 1) * 128 * 4;
       static int grid_per_sm = 0, sms = 0;
       if (!grid_per_sm) {
@@ -234,7 +247,7 @@ cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams
     }
   }
   dim3 grid((unsigned)((g.T - g.t_beg + 127) / 128), (unsigned)g.K);
-  return launch_pdl(k_output_xform<N, A, M, Tab>, grid, dim3(128), 0, s, Mx, y, g, xp);
+  return launch_pdl(k_output_xform<N, A, M, Tab, Ax>, grid, dim3(128), 0, s, Mx, y, g, xp);
 }
 
 template <int A, int M, class Tab>

@@ -1,4 +1,6 @@
 """GPU parity for per-axis transforms F(m_1 x .. x m_N, r_1 x .. x r_N)
+(the fused distinct-axis-0 kernels for F(2,3) x F(4,3)^2 and F(4,3) x F(2,3)^2,
+the generic multi-pass path for every other mix)
 (Eq. (4) indexes B_n, A_n, C_n by axis):
 wino_plan_create_nd against the float64 direct oracle on ragged shapes with
 padding, both GEMM schemes; e.g. F(2,3) along time with F(4,3) along space
@@ -70,6 +72,29 @@ def test_per_axis_parity(N, dims, m, r, pad, B, C, K, gemm_mode):
     assert rel <= tol and mx <= 10 * tol
 
 
+@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", [CASES[0], CASES[1],
+                                                   (3, (9, 30, 29), (2, 4, 4), (3, 3, 3), (1, 1, 1), 3, 20, 40)])
+def test_fused_mixed_axis0_equals_generic(N, dims, m, r, pad, B, C, K, monkeypatch):
+    # a distinct axis-0 F(m0, 3) over F(m, 3) on the other axes runs the fused
+    # kernels (xform_mixed.cu); the generic multi-pass path computes the same
+    # transforms with another summation order: both within tolerance, close
+    x, g = _inputs(dims, r, B, C, K, seed=5)
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), pad)
+    ys = []
+    for generic in ("0", "1"):
+        monkeypatch.setenv("WINO_ND_GENERIC", generic)
+        plan = pkg.Plan(N, dims, list(m), list(r), C, K, B, pad)
+        assert plan.info["axis_mode"] == (2 if generic == "1" else 1)
+        plan.filter_transform(g.cuda())
+        ys.append(plan.forward(x.cuda()).cpu().double().numpy())
+        plan.close()
+    tol = _tol(m, r)
+    for y in ys:
+        rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+        assert rel <= tol, rel
+    assert np.linalg.norm(ys[0] - ys[1]) / np.linalg.norm(ref) <= tol
+
+
 def test_per_axis_bias_relu_and_host_path():
     N, dims, m, r, pad, B, C, K = CASES[0]
     x, g = _inputs(dims, r, B, C, K, seed=3)
@@ -92,6 +117,7 @@ def test_equal_axes_take_the_fused_plan():
     x, g = _inputs((13, 11), (3, 3), 2, 8, 8)
     p1 = pkg.Plan(2, (13, 11), [4, 4], [3, 3], 8, 8, 2, (1, 1))
     p2 = pkg.Plan(2, (13, 11), 4, 3, 8, 8, 2, (1, 1))
+    assert p1.info["axis_mode"] == p2.info["axis_mode"] == 0
     for p in (p1, p2):
         p.filter_transform(g.cuda())
     assert torch.equal(p1.forward(x.cuda()), p2.forward(x.cuda()))
