@@ -481,15 +481,18 @@ def main():
             tk = traffic.get(name, {}).get(dom)
             if tk is not None:
                 rl["traffic"] = tk
-            per_stage = {s: {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
-                         for s, v in st.items() for rf in [roofline_for(r["cfg_local"], r["B"], s, v, peaks)]}
+            # a tiny plan runs the three stages in one kernel (timed as "gemm")
+            per_stage = {s: ({"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
+                             if v > 0 else {"ms": 0.0, "note": "fused into the single-kernel tiny path"})
+                         for s, v in st.items()
+                         for rf in [roofline_for(r["cfg_local"], r["B"], s, v, peaks) if v > 0 else None]}
             configs[name] = {"ms_per_layer": round(r["ms"], 5), "tflops_direct_equiv": round(r["tflops"], 2),
                              "stages": per_stage, "dominant": rl,
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
                                                                  "chunk_slabs", "gemm_variant", "in_slab_tiles",
-                                                                 "in_planes_per_cta")}}
+                                                                 "in_planes_per_cta", "axis_mode", "tiny")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
         if world == 1 and not args.no_cpu_baseline:

@@ -158,12 +158,13 @@ WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, fl
 WINO_API wino_status wino_plan_out_dims(wino_plan_t plan, int64_t* out);
 /* Device bytes: workspace (V + M) and filter buffer (U_hi + U_lo). */
 WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, size_t* filter_bytes);
-/* info[0..20): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
+/* info[0..21): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
  * (alpha^N), K_stride, gemm_mode, fuse, n_blk, k_chunk, chunk_slabs (0 =
  * unchunked), gemm_variant (0 SMEM-A, 1 TMEM-A, 2 CTA-pair; -1 FFMA; chosen by
  * timing the supported variants once in plan_create), input slab depth bt0,
  * input slabs per CTA npl, axis mode (0 one F(m, r) on every axis, 1 fused
- * kernels with a distinct axis-0 F(m0, r0), 2 generic per-axis passes). */
+ * kernels with a distinct axis-0 F(m0, r0), 2 generic per-axis passes), tiny
+ * (1: the whole forward runs in one kernel, chosen for tiny layers). */
 WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
 
 /* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------

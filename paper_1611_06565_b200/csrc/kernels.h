@@ -35,6 +35,11 @@ cudaError_t launch_input_mixed(int N, int alpha0, int m0, int alpha, int m, cons
                                const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
 cudaError_t launch_output_mixed(int N, int alpha0, int m0, int alpha, int m, const float* Mx, float* y,
                                 const KGeom& g, const XfParams& xp, const CUtensorMap* tmM, cudaStream_t s);
+// tiny layers: a2 + a3 + a4 in one kernel (xform_tiny.cu)
+bool tiny_shape(int N, int a, int C, int K, int64_t P, int* TB, int* smem);
+bool tiny_supported(int N, int a, int m);
+cudaError_t launch_tiny(const float* x, const float* Uhi, const float* Ulo, float* y, const KGeom& g,
+                        const XfParams& xp, int N, int a, int m, int spec, int P, int K_s, int64_t T, cudaStream_t s);
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s);
 

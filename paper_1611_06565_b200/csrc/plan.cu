@@ -201,6 +201,8 @@ struct wino_plan_s {
   // per-axis (m_n, r_n) plan (wino_plan_create_nd with unequal axes):
   // generic multi-pass transforms (xform_nd.cu), scratch W for the output passes
   bool nd = false;
+  // tiny layers: the whole forward in one kernel (xform_tiny.cu)
+  bool tiny = false;
   // fused plan with a distinct axis 0 (F(m0, r0); xform_mixed.cu)
   bool mixed = false;
   int m0 = 0, r0 = 0, a0 = 0;
@@ -403,6 +405,19 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
     }
+  }
+  {
+    // tiny layers (e.g. c1: 8x8, 4 -> 4 channels): one launch does a2 + a3
+    // + a4; fp32 FMA with U = U_hi + U_lo (3xTF32 plans only).  Opt-in
+    // (WINO_TINY=1): measured on c1 in CUDA-graph replay it takes 6.65 us
+    // per forward against 5.88 us for the three PDL-chained kernels.
+    // Decided on per-sample sizes and K <= 64 only, so batch shards and K
+    // shards of a tiny layer take the same path (reading #8)
+    int TB, smem;
+    const char* ev = getenv("WINO_TINY");
+    p->tiny = (ev && atoi(ev) != 0) && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32 &&
+              tiny_supported(N, a, m) && tiny_shape(N, a, C, K, p->P, &TB, &smem) && p->P * Tps * (int64_t)C <= 8192 &&
+              K <= 64;
   }
   *plan_out = p;
   return WINO_OK;
@@ -607,6 +622,15 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
   g.bias = bias;
   g.act = act;
   const bool rec = p->prof && p->prof_calls < kMaxProf;
+  if (p->tiny) {
+    ProfScope pt{p, s, 1};
+    if (rec) CUDA_TRY(pt.begin());
+    CUDA_TRY(launch_tiny(x, p->Uhi, p->Ulo, y, g, p->xp, p->N, p->a, p->m, p->spec, (int)p->P, (int)p->K_s,
+                         (int64_t)B * p->Tps, s));
+    if (rec) CUDA_TRY(pt.end());
+    if (rec) ++p->prof_calls;
+    return WINO_OK;
+  }
   if (p->nd) {
     // per-axis plan: generic multi-pass transforms around the same GEMM
     const int64_t T = (int64_t)B * p->Tps;
@@ -761,10 +785,10 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
-  const int64_t v[20] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[21] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
-                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0};
+                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

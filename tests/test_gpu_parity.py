@@ -319,3 +319,28 @@ def test_gemm_n_tile_choice_bit_identical(monkeypatch):
     x, g = make_inputs(cfg)
     rel, mx = errs(y.numpy(), direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad))
     assert rel <= 1e-5 and mx <= 1e-3
+
+
+@pytest.mark.parametrize("name,B", [("c1", 1), ("c2", 1), ("c5", 1)])
+def test_tiny_single_kernel_path(name, B, monkeypatch):
+    # tiny layers can run a2 + a3 + a4 in one kernel (opt-in WINO_TINY=1;
+    # fp32 FMA with U_hi + U_lo): within the BJ tolerance of the oracle
+    cfg = (CONFIGS if name == "c1" else SMALL)[name]
+    x, g = make_inputs(cfg, batch=B)
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad)
+    ys = {}
+    for tiny in ("1", "0"):
+        monkeypatch.setenv("WINO_TINY", tiny)
+        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding)
+        ys[tiny] = plan.info["tiny"]
+        plan.filter_transform(g.cuda())
+        y = plan.forward(x.cuda()).cpu().double().numpy()
+        yr = plan.forward(x.cuda(), bias=torch.ones(cfg.K).cuda(), relu=True).cpu().double().numpy()
+        plan.close()
+        rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+        tl, tm = tolerance(cfg)
+        assert rel <= tl and np.abs(y - ref).max() <= tm * np.abs(ref).max(), (tiny, rel)
+        assert np.allclose(yr, np.maximum(y + 1.0, 0.0), rtol=0, atol=1e-6)
+    assert ys["0"] == 0
+    if name == "c1":
+        assert ys["1"] == 1                      # BJ c1 qualifies for the single-kernel path
