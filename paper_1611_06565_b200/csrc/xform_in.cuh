@@ -89,8 +89,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     all_axes<A, 1, A, A, Get>(h, xp);
 #pragma unroll
     for (int j = 0; j < A; ++j) vout[j * pstride] = h[j];
-  } else if constexpr (N == 2) {
-    static_assert(Ax::A == A && Ax::M == M, "N = 2 whole-tile items need equal axes");
+  } else if constexpr (N == 2 && Ax::A == A && Ax::M == M) {
     // the whole alpha x alpha window in registers: every window row is read
     // once (no per-xi_0 re-reads), both axes transformed in place
     float h[A * A];
@@ -368,7 +367,9 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     }
   } else {
     // ---- work items (plane, xi_0, tile), tile fastest
-    constexpr int NX = N >= 3 ? Ax::A : 1;    // work items per tile (one per xi_0 when N >= 3)
+    // work items per tile: one per xi_0 when N >= 3 or when axis 0 has its
+    // own transform (N = 2 per-axis plans); one whole tile otherwise
+    constexpr int NX = (N >= 3 || Ax::A != A || Ax::M != M) ? Ax::A : 1;
     if (npl == 1) {
       // one plane: no plane index to decode (the common case for large slabs)
       ensure(0);

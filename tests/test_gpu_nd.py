@@ -72,7 +72,8 @@ def test_per_axis_parity(N, dims, m, r, pad, B, C, K, gemm_mode):
     assert rel <= tol and mx <= 10 * tol
 
 
-@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", [CASES[0], CASES[1],
+@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", [CASES[0], CASES[1], CASES[2],
+                                                   (2, (21, 30), (2, 4), (3, 3), (1, 1), 3, 12, 20),
                                                    (3, (9, 30, 29), (2, 4, 4), (3, 3, 3), (1, 1, 1), 3, 20, 40)])
 def test_fused_mixed_axis0_equals_generic(N, dims, m, r, pad, B, C, K, monkeypatch):
     # a distinct axis-0 F(m0, 3) over F(m, 3) on the other axes runs the fused
