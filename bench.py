@@ -56,7 +56,7 @@ def parse_args():
     ap.add_argument("--fuse", type=int, default=0, help="plan fuse bitmask (4 = L2-chunked a2->a3->a4)")
     ap.add_argument("--nets", default="fig4_f54,fig4_f34,fig3_f54",
                     help="the paper's own 2-D workloads (Figures 3 and 4) to time at N=1 ('' for none)")
-    ap.add_argument("--nd", default="c3t",
+    ap.add_argument("--nd", default="c3t,c3s133,c3t311",
                     help="per-axis F(m_1 x .. , r_1 x ..) workloads to time at N=1 ('' for none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the oracle sample")
@@ -336,6 +336,12 @@ def run_nets(args, local):
 ND_WORKLOADS = {
     "c3t": dict(N=3, dims=(16, 56, 56), m=(2, 4, 4), r=(3, 3, 3), pad=(1, 1, 1), B=16, C=64, K=128,
                 desc="c3 video layer 16x56x56, 16x64->128, F(2,3) time x F(4x4,3x3) space"),
+    # the (2+1)-D factorisation of the same layer: a 1x3x3 spatial and a
+    # 3x1x1 temporal convolution (anisotropic kernels; F(1,1) is the identity)
+    "c3s133": dict(N=3, dims=(16, 56, 56), m=(1, 4, 4), r=(1, 3, 3), pad=(0, 1, 1), B=16, C=64, K=128,
+                   desc="1x3x3 spatial kernel on c3's input, 16x64->128, F(1,1) x F(4x4,3x3)"),
+    "c3t311": dict(N=3, dims=(16, 56, 56), m=(4, 1, 1), r=(3, 1, 1), pad=(1, 0, 0), B=16, C=64, K=128,
+                   desc="3x1x1 temporal kernel on c3's input, 16x64->128, F(4,3) x F(1,1)^2"),
 }
 
 

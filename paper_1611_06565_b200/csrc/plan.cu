@@ -271,7 +271,9 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     spec0 = spec;
   }
   const int a = t.a, a0 = t0.a;
-  if (mixed && (spec == kSpecRuntime || spec0 == kSpecRuntime || points || fuse || !mixed_supported(N, a0, m0, a, m)))
+  // (mixed plans come from wino_plan_create_nd with default points on every
+  // axis: exactly the compile-time tables of xform_mixed.cu)
+  if (mixed && (points || fuse || !mixed_supported(N, a0, m0, a, m)))
     return fail(WINO_ERR_UNSUPPORTED, "no fused kernels for axis-0 F(%d,%d) with F(%d,%d) on N=%d", m0, r0, m, r, N);
   if (a > kMaxA || a0 > kMaxA || (!mixed && !xform_supported(N, a, m, spec)))
     return fail(WINO_ERR_UNSUPPORTED, "no device transform kernels for N=%d alpha=%d m=%d", N, a, m);
@@ -325,7 +327,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   }
   g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m;
   // the TMA slab needs 16-byte strides and the compile-time tables
-  const bool tma_shape = N >= 2 && spec != kSpecRuntime && (p->in[N - 1] % 4) == 0;
+  const bool tma_shape = N >= 2 && (spec != kSpecRuntime || mixed) && (p->in[N - 1] % 4) == 0;
   p->use_tma_in = p->use_tma_in && tma_shape;
   if (!plan_input_slab(g, N, a0, m0, a, m, p->use_tma_in)) {
     delete p;
@@ -449,7 +451,7 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   for (int n = 2; n < N; ++n) rest_equal = rest_equal && m[n] == m[1] && r[n] == r[1];
   const char* ev_gen = getenv("WINO_ND_GENERIC");
   if (rest_equal && !(ev_gen && atoi(ev_gen) != 0) && m[0] + r[0] - 1 <= kMaxA && m[1] + r[1] - 1 <= kMaxA &&
-      mixed_supported(N, m[0] + r[0] - 1, m[0], m[1] + r[1] - 1, m[1]) && r[0] == 3 && r[1] == 3)
+      mixed_supported(N, m[0] + r[0] - 1, m[0], m[1] + r[1] - 1, m[1]))
     return create_core(plan_out, N, dims, m[0], r[0], m[1], r[1], C, K, batch, padding, nullptr, gemm_mode, 0, device);
   Transforms tn[kMaxN];
   int64_t P = 1;

@@ -188,9 +188,11 @@ cudaError_t launch_input_nd(const float* x, float* V, const KGeom& g, const NdPa
   const unsigned bx = (unsigned)((t_hi - t_lo + 255) / 256);
   cudaError_t e = launch_pdl(k_nd_extract, dim3(bx, (unsigned)g.C, (unsigned)P), dim3(256), 0, s, x, V, g, q, N,
                              t_lo, t_hi);
-  for (int n = N - 1; n >= 0 && e == cudaSuccess; --n)
+  for (int n = N - 1; n >= 0 && e == cudaSuccess; --n) {
+    if (q.a[n] == 1 && q.BT[n][0][0] == 1.f) continue;  // r_n = m_n = 1: B_n^T = [1], nothing to do
     e = launch_pdl(k_nd_mode_in, dim3(bx, (unsigned)g.C, (unsigned)(P / q.a[n])), dim3(256), 0, s, V, g, q, N, n,
                    t_lo, t_hi);
+  }
   return e;
 }
 
@@ -204,6 +206,7 @@ cudaError_t launch_output_nd(const float* Mx, float* W, float* y, const KGeom& g
   int which = 0;
   cudaError_t e = cudaSuccess;
   for (int n = N - 1; n >= 1 && e == cudaSuccess; --n) {
+    if (ein[n] == 1 && q.m[n] == 1 && q.AT[n][0][0] == 1.f) continue;  // A_n^T = [1]
     int lines = 1;
     for (int j = 0; j < N; ++j)
       if (j != n) lines *= ein[j];

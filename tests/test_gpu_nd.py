@@ -33,6 +33,9 @@ CASES = [
     (3, (6, 11, 12), (1, 4, 4), (1, 3, 3), (0, 1, 1), 2, 8, 16),      # 1x3x3 (2-D kernels in a 3-D net)
     (4, (4, 5, 6, 7), (2, 2, 3, 2), (3, 2, 2, 3), (1, 0, 0, 1), 2, 4, 6),
     (1, (40,), (5,), (4,), (2,), 2, 6, 7),                            # N = 1 (uniform: fused path)
+    (3, (6, 13, 12), (2, 1, 1), (3, 1, 1), (1, 0, 0), 2, 8, 8),      # 3x1x1 temporal kernel
+    (3, (5, 12, 16), (1, 2, 2), (1, 3, 3), (0, 1, 1), 2, 8, 8),      # 1x3x3 with F(2,3) spatial
+    (2, (14, 12), (4, 1), (3, 1), (1, 0), 2, 8, 8),                   # 3x1
 ]
 
 
@@ -72,7 +75,8 @@ def test_per_axis_parity(N, dims, m, r, pad, B, C, K, gemm_mode):
     assert rel <= tol and mx <= 10 * tol
 
 
-@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", [CASES[0], CASES[1], CASES[2],
+@pytest.mark.parametrize("N,dims,m,r,pad,B,C,K", [CASES[0], CASES[1], CASES[2], CASES[5], CASES[8], CASES[9],
+                                                   CASES[10],
                                                    (2, (21, 30), (2, 4), (3, 3), (1, 1), 3, 12, 20),
                                                    (3, (9, 30, 29), (2, 4, 4), (3, 3, 3), (1, 1, 1), 3, 20, 40)])
 def test_fused_mixed_axis0_equals_generic(N, dims, m, r, pad, B, C, K, monkeypatch):
