@@ -365,6 +365,46 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
 #pragma unroll
       for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
     }
+  } else if constexpr (A == 1 && M == 1 && N >= 2) {
+    // ---- r = 1 on every axis but 0 (3x1x1-type kernels): a tile is one
+    // pixel column; one work item per (plane, depth tile, pixel) reads the
+    // alpha_0 values along axis 0 (lanes = consecutive pixels: conflict-free
+    // loads, coalesced stores) and writes all alpha_0 points
+    using Get0 = BTget<typename Ax::Tab>;
+    constexpr int A0 = Ax::A, M0 = Ax::M;
+    const int R = g.R, nper = g.bt0 * R;
+    for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
+      const int p = u / nper;
+      const int w = u - p * nper;
+      const int t0l = w / R, rr = w - t0l * R;
+      if (t0l >= pl[p].nt0) continue;
+      ensure(p);
+      int rem = rr, off = t0l * M0 * g.sst[0];
+#pragma unroll
+      for (int ax = N - 1; ax >= 1; --ax) {
+        const int ti = rem % g.tiles[ax];
+        rem /= g.tiles[ax];
+        off += ti * g.sst[ax];
+      }
+      const float* col = S0 + p * slab_f + off + D;
+      float v[A0];
+#pragma unroll
+      for (int i = 0; i < A0; ++i) v[i] = col[i * g.sst[0]];
+      float* vo = vbase(p) + w;
+#pragma unroll
+      for (int x0 = 0; x0 < A0; ++x0) {
+        float acc = 0.f;
+        bool first = true;
+#pragma unroll
+        for (int i = 0; i < A0; ++i) {
+          if (Get0::nz(xp, x0, i)) {
+            acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
+            first = false;
+          }
+        }
+        vo[x0 * pstride] = acc;
+      }
+    }
   } else {
     // ---- work items (plane, xi_0, tile), tile fastest
     // work items per tile: one per xi_0 when N >= 3 or when axis 0 has its
