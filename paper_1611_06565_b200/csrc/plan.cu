@@ -402,7 +402,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   if (tc) {
     e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
                         p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
-    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K);
+    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K, p->V);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
@@ -543,7 +543,7 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   if (tc) {
     e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)P, p->T_s, C, (int)p->K_s, K,
                         p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
-    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)P, T, p->T_s, C, K);
+    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)P, T, p->T_s, C, K, p->V);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
