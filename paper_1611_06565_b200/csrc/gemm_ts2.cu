@@ -360,6 +360,8 @@ static bool ts2_smem(int bn, int kc, int* nraw, int* nbr, size_t* bytes) {
   const size_t fixed = 1024 + 1024;
   const size_t budget = 232448;
   size_t left = budget - fixed;
+  // 4 U stages: measured (tools/pair_ring.sh) 6 or 8 give the same GEMM time
+  // and a slower three-kernel step (c2 0.103 -> 0.109, c3 1.74 -> 1.89 ms)
   int nb = 4;
   while (nb > 2 && nb * hb2 + 4 * a > left) --nb;
   if (nb * hb2 + 2 * a > left) return false;
