@@ -135,3 +135,28 @@ def test_per_axis_errors():
         pkg.Plan(2, (16, 16), [6, 2], [4, 3], 4, 4, 1, (1, 1))
     with pytest.raises(ValueError):                    # points / fusion not per axis
         pkg.Plan(2, (16, 16), [2, 4], [3, 3], 4, 4, 1, (1, 1), fuse=4)
+
+
+@pytest.mark.parametrize("name", ["c3t", "c3s133", "c3t311"])
+def test_bench_per_axis_workloads_full_size_sampled(name):
+    # the bench's per-axis workloads at full size, in the bench's launch
+    # configuration: 4096 random outputs plus the first / last 64, each
+    # computed one by one by the float64 oracle
+    import bench
+    w = bench.ND_WORKLOADS[name]
+    gen = torch.Generator("cpu").manual_seed(0)
+    x = torch.randn((w["B"], w["C"]) + w["dims"], generator=gen)
+    g = torch.randn((w["K"], w["C"]) + w["r"], generator=gen) * math.sqrt(2.0 / (w["C"] * math.prod(w["r"])))
+    plan = pkg.Plan(w["N"], w["dims"], list(w["m"]), list(w["r"]), w["C"], w["K"], w["B"], w["pad"])
+    assert plan.info["axis_mode"] == 1
+    plan.filter_transform(g.cuda())
+    y = plan.forward(x.cuda()).cpu().double().numpy()
+    plan.close()
+    rng = np.random.default_rng(2)
+    idx = np.concatenate([np.arange(64), np.arange(y.size - 64, y.size), rng.integers(0, y.size, 4096)])
+    ref = direct.direct_conv_at(x.numpy(), g.numpy(), w["pad"], idx)
+    got = y.reshape(-1)[idx]
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    tol = _tol(w["m"], w["r"])
+    print("%s sampled relL2=%.2e tol=%.1e" % (name, rel, tol))
+    assert rel <= tol and np.abs(got - ref).max() <= 10 * tol * np.abs(ref).max()

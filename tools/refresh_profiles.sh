@@ -15,6 +15,10 @@ for c in c2 c3 c4 c5; do
     python bench.py --steps 2 --warmup 3 --config $c --extra "" --nets "" --no-cpu-baseline > /tmp/${T}_$c.log 2>&1; echo ncu_$c=$?
   ncu -i /tmp/${T}_$c.ncu-rep --page raw --csv > gpurun_out/${T}_${c}_raw.csv
 done
+# the per-axis c3 layer (F(2,3) time x F(4,3)^2 space): its three fused kernels
+timeout 600 ncu -f --set full --import-source on --clock-control none -k regex:"k_input|k_gemm|k_output" -s 5 -c 3 \
+  -o /tmp/${T}_c3t python tools/run_nd.py c3t 3 > /tmp/${T}_c3t.log 2>&1; echo ncu_c3t=$?
+ncu -i /tmp/${T}_c3t.ncu-rep --page raw --csv > gpurun_out/${T}_c3t_raw.csv
 read V BN <<< $(python -c "import json; d=json.load(open('gpurun_out/${T}_bench.json'))['configs']['c2']['info']; print(d['gemm_variant'], d['n_blk'])")
 WINO_GEMM_VARIANT=$V WINO_GEMM_BN=$BN timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${T}_launches_c2.csv python bench.py --steps 3 --warmup 3 --extra "" --nets "" --no-cpu-baseline \
