@@ -16,8 +16,9 @@ for c in c2 c3 c4 c5; do
   ncu -i /tmp/${T}_$c.ncu-rep --page raw --csv > gpurun_out/${T}_${c}_raw.csv
 done
 # the per-axis c3 layer (F(2,3) time x F(4,3)^2 space): its three fused kernels
-timeout 600 ncu -f --set full --import-source on --clock-control none -k regex:"k_input|k_gemm|k_output" -s 5 -c 3 \
-  -o /tmp/${T}_c3t python tools/run_nd.py c3t 3 > /tmp/${T}_c3t.log 2>&1; echo ncu_c3t=$?
+VT=$(python tools/run_nd.py c3t 1 | awk '{print $3}')
+WINO_GEMM_VARIANT=$VT timeout 600 ncu -f --set full --import-source on --clock-control none -k regex:"k_input|k_gemm|k_output" -c 3 \
+  -o /tmp/${T}_c3t python tools/run_nd.py c3t 3 > /tmp/${T}_c3t.log 2>&1; echo ncu_c3t=$? variant=$VT
 ncu -i /tmp/${T}_c3t.ncu-rep --page raw --csv > gpurun_out/${T}_c3t_raw.csv
 read V BN <<< $(python -c "import json; d=json.load(open('gpurun_out/${T}_bench.json'))['configs']['c2']['info']; print(d['gemm_variant'], d['n_blk'])")
 WINO_GEMM_VARIANT=$V WINO_GEMM_BN=$BN timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
