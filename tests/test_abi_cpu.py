@@ -100,3 +100,21 @@ def test_plan_without_device_fails_loudly():
     with pytest.raises(pkg.WinoError) as ei:
         pkg.Plan(2, (8, 8), 2, 3, 4, 4, 1)
     assert ei.value.status in (wino.WINO_ERR_CUDA, wino.WINO_ERR_NOMEM)
+
+
+def test_per_axis_plan_argument_errors():
+    # wino_plan_create_nd validates before touching the device
+    cases = [
+        (dict(N=5, dims=(8,) * 5, m=(2,) * 5, r=(3,) * 5, padding=(1,) * 5), wino.WINO_ERR_ARG),
+        (dict(m=(6, 2), r=(4, 3)), wino.WINO_ERR_UNSUPPORTED),     # alpha_0 = 9 > 8
+        (dict(m=(2, 0), r=(3, 3)), wino.WINO_ERR_ARG),             # m_1 = 0
+        (dict(dims=(2, 8), m=(2, 4), r=(3, 3), padding=(0, 1)), wino.WINO_ERR_SHAPE),   # kernel > input on axis 0
+        (dict(C=0), wino.WINO_ERR_ARG),
+    ]
+    for kw, status in cases:
+        args = dict(N=2, dims=(8, 8), m=(2, 4), r=(3, 3), C=4, K=4, batch=1, padding=(1, 1))
+        args.update(kw)
+        with pytest.raises(pkg.WinoError) as ei:
+            pkg.wino_plan_create_nd(args["N"], args["dims"], args["m"], args["r"], args["C"], args["K"],
+                                    args["batch"], args["padding"])
+        assert ei.value.status == status, pkg.wino_last_error()
