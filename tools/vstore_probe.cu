@@ -74,6 +74,23 @@ __global__ void __launch_bounds__(384) k4(float* V, int run, int P, int C, long 
   }
 }
 
+// k2 with a per-slab t stride `pitch` >= run (pitch = run: packed, current
+// layout; pitch = run rounded up to 8 floats: 32-byte aligned runs)
+__global__ void __launch_bounds__(256) k5(float* V, int run, int pitch, int P, int C, long long T_s, int nslab_per_c) {
+  const int w = blockIdx.x;
+  const int c = w / nslab_per_c;
+  const long long t0 = (long long)(w % nslab_per_c) * pitch;
+  const long long pstride = (long long)C * T_s;
+  float* vb = V + (long long)c * T_s + t0;
+  const int A2 = 36, A = 6;
+  for (int it = threadIdx.x; it < A * run; it += blockDim.x) {
+    const int xi0 = it / run, tl = it - xi0 * run;
+    float* vo = vb + tl + (long long)xi0 * A2 * pstride;
+#pragma unroll
+    for (int j = 0; j < A2; ++j) vo[j * pstride] = (float)j;
+  }
+}
+
 int main() {
   const int P = 216, C = 256, B = 32, Tps = 98;
   const long long T = (long long)B * Tps, T_s = (T + 127) / 128 * 128;
@@ -113,6 +130,24 @@ int main() {
     ms /= 5;
     printf("k3 nsub %d (CTA loops over 49-tile slabs): %.1f us  %.0f GB/s\n", nsub, ms * 1e3,
            (double)P * C * T * 4 / (ms * 1e-3) / 1e9);
+  }
+  for (int pitch : {98, 104, 128}) {
+    const int run = 98;
+    const long long Tp = (long long)B * pitch, T_sp = (Tp + 127) / 128 * 128;
+    float* V2;
+    cudaMalloc(&V2, (size_t)P * C * T_sp * 4);
+    const int nslab_per_c = B;
+    const int grid = nslab_per_c * C;
+    for (int w = 0; w < 2; ++w) k5<<<grid, 256>>>(V2, run, pitch, P, C, T_sp, nslab_per_c);
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; ++r) k5<<<grid, 256>>>(V2, run, pitch, P, C, T_sp, nslab_per_c);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= 5;
+    printf("k5 run 98 pitch %d: %.1f us  %.0f GB/s of V\n", pitch, ms * 1e3, (double)P * C * T * 4 / (ms * 1e-3) / 1e9);
+    cudaFree(V2);
   }
   for (int run : {49, 98}) {
     const int nslab_per_c = (int)(T / run);
