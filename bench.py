@@ -345,7 +345,7 @@ ND_WORKLOADS = {
 }
 
 
-def run_nd(args, local):
+def run_nd(args, local, peaks=None):
     import torch
     import paper_1611_06565_b200 as pkg
     dev = torch.device("cuda", local)
@@ -383,11 +383,22 @@ def run_nd(args, local):
         stage_ms, calls = plan.profile_read()
         plan.profile(False)
         flops = 2 * w["B"] * w["K"] * w["C"] * math.prod(plan.out_dims) * math.prod(w["r"])
+        # per-stage roofline fractions from the cost model's compulsory bytes / flops
+        from paper_1611_06565_b200.cost import stage_model
+        pk = peaks or load_peaks()
+        tf32 = pk["bf16"] * GUIDE_TF32_OVER_BF16
+        sm = stage_model(w["N"], w["dims"], w["m"], w["r"], w["C"], w["K"], w["B"], w["pad"],
+                         hbm_gbs=pk["hbm_gbs"], tf32_tflops=tf32)
+        frac = {}
+        for sname, v in zip(["input_xform", "gemm", "output_xform"], stage_ms):
+            t_ms = v / calls
+            frac[sname] = round(sm[sname]["roofline_ms"] / t_ms, 3) if t_ms > 0 else None
         out[name] = {"desc": w["desc"], "F": "F(%s, %s)" % ("x".join(map(str, w["m"])), "x".join(map(str, w["r"]))),
                      "ms_per_layer": round(ms, 4), "tflops_direct_equiv": round(flops / (ms * 1e-3) / 1e12, 2),
                      "n_points": plan.info["n_points"],
                      "stages_ms": {s: round(v / calls, 4) for s, v in
                                    zip(["input_xform", "gemm", "output_xform"], stage_ms)},
+                     "stages_roofline_frac": frac,
                      "path": {0: "single F(m, r) fused kernels",
                               1: "fused kernels with a distinct axis-0 transform (xform_mixed.cu)",
                               2: "generic multi-pass per-axis transforms (xform_nd.cu)"}[plan.info["axis_mode"]]
@@ -515,7 +526,7 @@ def main():
         if world == 1 and args.nets:
             out["paper_workloads"] = run_nets(args, local)
         if world == 1 and args.nd:
-            out["per_axis_workloads"] = run_nd(args, local)
+            out["per_axis_workloads"] = run_nd(args, local, peaks)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -46,6 +46,15 @@ def theoretical_speedup(S: int, G: int, N: int) -> Fraction:
     return Fraction(S * G, S + G - 1) ** N
 
 
+def theoretical_speedup_axes(S: Sequence[int], G: Sequence[int]) -> Fraction:
+    """prod_n S_n G_n / D_n for per-axis transforms (Eq. (4) applies one
+    F(S_n, G_n) per axis; the N-D count factorises over the axes)."""
+    out = Fraction(1)
+    for s_, g_ in zip(S, G):
+        out *= theoretical_speedup(s_, g_, 1)
+    return out
+
+
 def direct_muls(M: int, K: int, S: int, G: int, N: int) -> int:
     """Sliding-window multiplications for one S^N output tile, all M x K pairs."""
     return M * K * S ** N * G ** N
@@ -101,24 +110,26 @@ def arithmetic_intensity(T: int, M: int, K: int, fused: bool) -> Fraction:
 
 
 # ------------------------------------------------------------------ device
-def stage_model(N: int, dims: Sequence[int], m: int, r: int, C: int, K: int, B: int,
+def stage_model(N: int, dims: Sequence[int], m, r, C: int, K: int, B: int,
                 pad: Sequence[int] = None, hbm_gbs: float = None, tf32_tflops: float = None) -> Dict[str, dict]:
     """Algorithmic bytes / flops of the four stages of one forward (fp32,
     every tensor moved once) and, if peaks are given, the
     roofline time in ms of each stage (the GEMM at the 3xTF32 rate =
-    tf32_tflops / 3 fp32-equivalent)."""
+    tf32_tflops / 3 fp32-equivalent).  m and r may be per-axis sequences
+    (F(m_1 x .. x m_N, r_1 x .. x r_N), Eq. (4))."""
     pad = tuple(pad) if pad is not None else (0,) * N
-    a = m + r - 1
-    out = [d + 2 * p - r + 1 for d, p in zip(dims, pad)]
-    T = B * math.prod(-(-o // m) for o in out)
-    P = a ** N
+    mv = tuple(m) if isinstance(m, (list, tuple)) else (m,) * N
+    rv = tuple(r) if isinstance(r, (list, tuple)) else (r,) * N
+    out = [d + 2 * p - rn + 1 for d, p, rn in zip(dims, pad, rv)]
+    T = B * math.prod(-(-o // mn) for o, mn in zip(out, mv))
+    P = math.prod(mn + rn - 1 for mn, rn in zip(mv, rv))
     xb = 4 * B * C * math.prod(dims)
     yb = 4 * B * K * math.prod(out)
     # U counted once in fp32 (the compulsory filter bytes; the 3xTF32 GEMM
     # streams its hi/lo halves, i.e. 2x this, from L2)
     Vb, Mb, Ub = 4 * P * C * T, 4 * P * K * T, 4 * P * C * K
     st = {
-        "filter_xform": {"bytes": 4 * K * C * r ** N + Ub, "flops": 0},
+        "filter_xform": {"bytes": 4 * K * C * math.prod(rv) + Ub, "flops": 0},
         "input_xform": {"bytes": xb + Vb, "flops": 0},
         "gemm": {"bytes": Vb + Ub + Mb, "flops": 2 * P * T * C * K},
         "output_xform": {"bytes": Mb + yb, "flops": 0},
@@ -129,7 +140,7 @@ def stage_model(N: int, dims: Sequence[int], m: int, r: int, C: int, K: int, B: 
             t_tc = s["flops"] / (tf32_tflops / 3 * 1e12) if (tf32_tflops and s["flops"]) else 0.0
             s["roofline_ms"] = 1e3 * max(t_mem, t_tc)
             s["bound"] = "tensor" if t_tc > t_mem else "hbm"
-    st["direct_flops"] = 2 * B * K * C * math.prod(out) * r ** N
+    st["direct_flops"] = 2 * B * K * C * math.prod(out) * math.prod(rv)
     st["tiles"] = T
     return st
 

@@ -141,3 +141,20 @@ def test_cli_runs(capsys):
     out = capsys.readouterr().out.strip().splitlines()
     assert out[1].startswith("M,K,direct_muls")
     assert out[2].split(",")[:5] == ["1", "1", "6", "28", "18"]
+
+
+def test_per_axis_speedup_and_bytes():
+    # equal axes reduce to (SG/D)^N; F(2,3) x F(4,3)^2: 1.5 * 2 * 2
+    assert cost.theoretical_speedup_axes((4, 4, 4), (3, 3, 3)) == cost.theoretical_speedup(4, 3, 3)
+    assert cost.theoretical_speedup_axes((2, 4, 4), (3, 3, 3)) == Fraction(3, 2) * 2 * 2
+    assert cost.theoretical_speedup_axes((1, 4, 4), (1, 3, 3)) == 4        # 1x3x3: F(1,1) gains nothing
+    st = cost.stage_model(3, (16, 56, 56), (2, 4, 4), (3, 3, 3), 64, 128, 16, (1, 1, 1))
+    T = 16 * 8 * 14 * 14
+    assert st["tiles"] == T
+    assert st["input_xform"]["bytes"] == 4 * 16 * 64 * 16 * 56 * 56 + 4 * 144 * 64 * T
+    assert st["gemm"]["flops"] == 2 * 144 * T * 64 * 128
+    assert st["direct_flops"] == 2 * 16 * 128 * 64 * 16 * 56 * 56 * 27
+    # uniform sequences equal the scalar form
+    a = cost.stage_model(2, (56, 56), 4, 3, 128, 128, 32, (1, 1))
+    b = cost.stage_model(2, (56, 56), (4, 4), (3, 3), 128, 128, 32, (1, 1))
+    assert a == b
