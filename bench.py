@@ -203,6 +203,7 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if rank == 0 or ksplit:
             gd = g.to(dev)
+            plan.filter_transform(gd, stream)          # first call (module load), then timed
             e0.record(stream)
             plan.filter_transform(gd, stream)
             e1.record(stream)

@@ -1,6 +1,8 @@
 // xform_out.cu -- host dispatch of stage a4 and stage a1, the filter
 // transform:  U_xi[c][k] = (g[k, c] x_1 G ... x_N G)_xi  (Eq. (4),
 // PAPER.md:160-164; cached transformed kernels PAPER.md:178).
+#include <cstdlib>
+
 #include "kernels.h"
 #include "tma.hpp"
 #include "xform_out.cuh"
@@ -79,8 +81,74 @@ bool encode_output_map(CUtensorMap* tm, const float* Mx, int64_t T_s, int K, int
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Blocked form of the same sum: a CTA owns (c, 64 kernels k); the weights
+// W[xi][p] = prod_n G_n[xi_n][p_n] (fp64) and the 64 kernels' taps g[k][c][:]
+// are staged in shared memory once, then U[xi][c][k] = sum_p W[xi][p] g[k,c,p]
+// with lanes = consecutive k (coalesced U stores, W broadcast).  Same fp64
+// products and summation order (p ascending) as k_filter_xform: identical bits.
+constexpr int kFiltKB = 64;
+__global__ void __launch_bounds__(256)
+k_filter_xform_blk(const float* __restrict__ g, float* __restrict__ Uhi, float* __restrict__ Ulo,
+                   float* __restrict__ U32, const __grid_constant__ FParams fp, int rN) {
+  extern __shared__ double fsm[];
+  double* W = fsm;                              // [P][rN]
+  float* gs = reinterpret_cast<float*>(W + fp.P * rN);  // [kFiltKB][rN]
+  const int c = blockIdx.x;
+  const int k0 = blockIdx.y * kFiltKB;
+  const int P = (int)fp.P;
+  for (int i = threadIdx.x; i < P * rN; i += blockDim.x) {
+    const int xi = i / rN, p = i - xi * rN;
+    int q = xi, pq = p;
+    double w = 1.0;
+    for (int n = fp.N - 1; n >= 0; --n) {
+      w *= fp.G[n][q % fp.a[n]][pq % fp.r[n]];
+      q /= fp.a[n];
+      pq /= fp.r[n];
+    }
+    W[i] = w;
+  }
+  for (int i = threadIdx.x; i < kFiltKB * rN; i += blockDim.x) {
+    const int kl = i / rN, p = i - kl * rN;
+    const int k = k0 + kl;
+    gs[i] = k < fp.K ? __ldg(g + ((int64_t)k * fp.C + c) * rN + p) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P * kFiltKB; i += blockDim.x) {
+    const int xi = i / kFiltKB, kl = i - xi * kFiltKB;
+    const int k = k0 + kl;
+    if (k >= fp.K_s) continue;
+    float u = 0.f;
+    if (k < fp.K) {
+      const double* wr = W + xi * rN;
+      const float* gr = gs + kl * rN;
+      double acc = 0.0;
+      for (int p = 0; p < rN; ++p)
+        if (wr[p] != 0.0) acc = fma(wr[p], (double)gr[p], acc);
+      u = (float)acc;
+    }
+    const int64_t at = ((int64_t)xi * fp.C + c) * fp.K_s + k;
+    const float hi = tf32_rna(u);
+    if (Uhi) Uhi[at] = hi;
+    if (Ulo) Ulo[at] = tf32_rna(u - hi);
+    if (U32) U32[at] = u;
+  }
+}
+
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s) {
+  int rN = 1;
+  for (int n = 0; n < fp.N; ++n) rN *= fp.r[n];
+  const size_t smem = (size_t)fp.P * rN * 8 + (size_t)kFiltKB * rN * 4;
+  const char* ev = getenv("WINO_FILTER_BLK");  // 0: the per-output kernel (tests compare both)
+  if ((!ev || atoi(ev) != 0) && smem <= 100 * 1024 && fp.C <= 65535) {
+    if (smem > 46 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_filter_xform_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    dim3 grid((unsigned)fp.C, (unsigned)((fp.K_s + kFiltKB - 1) / kFiltKB));
+    k_filter_xform_blk<<<grid, 256, smem, s>>>(g, Uhi, Ulo, U32, fp, rN);
+    return cudaGetLastError();
+  }
   const int64_t n = (int64_t)fp.C * fp.K_s;
   dim3 grid((unsigned)((n + 255) / 256), (unsigned)fp.P);
   k_filter_xform<<<grid, 256, 0, s>>>(g, Uhi, Ulo, U32, fp);

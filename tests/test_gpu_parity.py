@@ -344,3 +344,20 @@ def test_tiny_single_kernel_path(name, B, monkeypatch):
     assert ys["0"] == 0
     if name == "c1":
         assert ys["1"] == 1                      # BJ c1 qualifies for the single-kernel path
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_filter_transform_blocked_matches_per_output(name, monkeypatch):
+    # a1's blocked kernel (W and the taps staged in shared memory) and the
+    # per-output kernel form the same fp64 products in the same order
+    cfg = SMALL[name]
+    x, g = make_inputs(cfg)
+    bufs = []
+    for blk in ("1", "0"):
+        monkeypatch.setenv("WINO_FILTER_BLK", blk)
+        plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, cfg.batch, cfg.padding)
+        plan.filter_transform(g.cuda())
+        torch.cuda.synchronize()
+        bufs.append(plan.filter_tensor().clone().cpu())
+        plan.close()
+    assert torch.equal(bufs[0], bufs[1])
