@@ -326,8 +326,8 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     sin *= p->in[n]; sout *= p->out[n];
   }
   g.in_vol = sin; g.out_vol = sout; g.Tps = Tps; g.T = T; g.T_s = p->T_s; g.C = C; g.K = K; g.m = m;
-  // the TMA slab needs 16-byte strides and the compile-time tables
-  const bool tma_shape = N >= 2 && (spec != kSpecRuntime || mixed) && (p->in[N - 1] % 4) == 0;
+  // the TMA slab needs 16-byte row strides (and a supported column shift, see encode_input_map)
+  const bool tma_shape = N >= 2 && (p->in[N - 1] % 4) == 0;
   p->use_tma_in = p->use_tma_in && tma_shape;
   if (!plan_input_slab(g, N, a0, m0, a, m, p->use_tma_in)) {
     delete p;

@@ -114,7 +114,7 @@ bool encode_input_map(CUtensorMap* tm, const float* x, const KGeom& g, int N, in
 cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
                                const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s) {
   if (spec != kSpecRuntime) return launch_input_const(N, alpha, m, spec, x, V, g, xp, tm, nslab, s);
-  return launch_input_run(N, alpha, m, x, V, g, xp, nslab, s);
+  return launch_input_run(N, alpha, m, x, V, g, xp, tm, nslab, s);
 }
 
 }  // namespace wino

@@ -557,6 +557,6 @@ cudaError_t launch_in_byN(int N, const float* x, float* V, const KGeom& g, const
 cudaError_t launch_input_const(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
                                const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s);
 cudaError_t launch_input_run(int N, int alpha, int m, const float* x, float* V, const KGeom& g, const XfParams& xp,
-                             int nslab, cudaStream_t s);
+                             const CUtensorMap* tm, int nslab, cudaStream_t s);
 
 }  // namespace wino

@@ -56,3 +56,24 @@ def test_unsupported_alpha_is_an_error():
     with pytest.raises(pkg.WinoError) as ei:
         pkg.Plan(2, (16, 16), 4, 4, 4, 4, 1, (1, 1))
     assert ei.value.status == pkg.wino.WINO_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("N,dims,m,r,pad", [(2, (20, 24), 5, 4, 1), (2, (19, 28), 5, 4, 0), (1, (44,), 5, 4, 1),
+                                             (3, (5, 7, 8), 4, 5, 1), (2, (14, 16), 3, 6, 1)])
+def test_runtime_tables_tma_slab_matches_cp_async(N, dims, m, r, pad, monkeypatch):
+    # alpha = 8 run-time-table plans take the TMA slab load when the last
+    # extent is a multiple of 4 floats: same bits as the cp.async fallback
+    cfg = LayerConfig("mrt", N, 2, 6, 7, dims, r, pad, m, "normal", "he")
+    x, g = make_inputs(cfg)
+    ys = []
+    for tma in ("1", "0"):
+        monkeypatch.setenv("WINO_IN_TMA", tma)
+        plan = pkg.Plan(N, dims, m, r, cfg.C, cfg.K, cfg.batch, cfg.padding)
+        plan.filter_transform(g.cuda())
+        ys.append(plan.forward(x.cuda()).cpu())
+        plan.close()
+    assert torch.equal(ys[0], ys[1])
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad)
+    y = ys[0].double().numpy()
+    rel = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    assert rel <= 4e-7 * GROWTH[m + r - 1] ** N
