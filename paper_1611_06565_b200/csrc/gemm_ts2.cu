@@ -73,6 +73,25 @@ __device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap
       "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(cl_bar)
       : "memory");
 }
+// L2 eviction-priority policies (createpolicy) and hinted accesses: V is
+// streamed once (evict-first), M is read right after by a4 (evict-last).
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+  uint64_t pol;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                                 uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tc2_commit_mc(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
@@ -97,7 +116,7 @@ template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
 k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
            const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-           int C, int K, int kc, int three, int nraw, int nbr, int dbg) {
+           int C, int K, int kc, int three, int nraw, int nbr, int dbg, int l2hint) {
   constexpr int HN = BN / 2;  // U columns loaded by each CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
@@ -183,7 +202,8 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             mbar_arrive(rfull(s));  // dev knob: no V loads
           } else {
             mbar_expect_tx(rfull(s), a_bytes);
-            tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * kc, xi, rfull(s));
+            if (l2hint) tma_load_3d_hint(raw0 + s * a_bytes, &tmA, row0, ch * kc, xi, rfull(s), l2_policy(false));
+            else tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * kc, xi, rfull(s));
           }
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
@@ -319,7 +339,15 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T && !(dbg & 1)) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (full_n) {
+          if (l2hint) {  // M stays in L2 for a4
+            const uint64_t pol = l2_policy(true);
+            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
+              p += T_s;
+            }
+          } else if (full_n) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               __stcs(p, __uint_as_float(r[j]));
@@ -421,10 +449,18 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
     fprintf(stderr, "[wino] k_gemm_ts2<%d>: max co-resident pairs %d, units %lld, nraw %d, nbr %d, smem %zu\n", BN,
             max_pairs, units, nraw, nbr, smem);
   if (pairs > units) pairs = units;
+  // L2 policies: V loads evict-first (streamed once), M stores evict-last (a4
+  // reads M right after).  Measured: c2 0.103 -> 0.100 ms, c3 1.747 -> 1.713
+  // ms per layer (a4 33.1 -> 31.1 us on c2).  WINO_L2_HINTS=0 disables.
+  static int l2hint = -1;
+  if (l2hint < 0) {
+    const char* ev = getenv("WINO_L2_HINTS");
+    l2hint = ev ? (atoi(ev) != 0) : 1;
+  }
   if (pairs < 1) return cudaSuccess;
   const long long Ts = T_s;
   return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P,
-                    t_lo, T, Ts, C, K, tg.kc, tg.three, nraw, nbr, tg.dbg);
+                    t_lo, T, Ts, C, K, tg.kc, tg.three, nraw, nbr, tg.dbg, l2hint);
 }
 
 cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
