@@ -47,7 +47,7 @@ template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-          int C, int K, int kc, int three, int nraw, int nop, int nbr) {
+          int C, int K, int kc, int three, int nraw, int nop, int nbr, int l2hint) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
@@ -144,7 +144,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(rfull(s), a_bytes);
 #pragma unroll
           for (int gq = 0; gq < BM / 32; ++gq)
-            tma_load_3d(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, rfull(s));
+            if (l2hint)
+              tma_load_3d_hint(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, rfull(s),
+                               l2_policy(false));
+            else
+              tma_load_3d(st + gq * kc * 128, &tmA, t_lo + mb * BM + gq * 32, ch * kc, xi, rfull(s));
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
       }
@@ -312,7 +316,15 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (full_n) {
+          if (l2hint) {  // M stays in L2 for a4 (evict-last)
+            const uint64_t pol = l2_policy(true);
+            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
+              p += T_s;
+            }
+          } else if (full_n) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               __stcs(p, __uint_as_float(r[j]));
@@ -356,7 +368,7 @@ template <int BN, bool kRes>
 __global__ void __launch_bounds__(kThreadsTS, 1)
 k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
           const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-          int C, int K, int kc, int three, int nraw, int nbr, int dbg) {
+          int C, int K, int kc, int three, int nraw, int nbr, int dbg, int l2hint) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
@@ -452,7 +464,10 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             mbar_arrive(rfull(s));  // dev knob: no V loads
           } else {
             mbar_expect_tx(rfull(s), a_bytes);
-            tma_load_3d(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s));
+            if (l2hint)
+              tma_load_3d_hint(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s), l2_policy(false));
+            else
+              tma_load_3d(raw0 + s * a_bytes, &tmA, t_lo + mb * BM, ch * kc, xi, rfull(s));
           }
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
@@ -624,7 +639,15 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T && !(dbg & 1)) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (full_n) {
+          if (l2hint) {  // M stays in L2 for a4 (evict-last)
+            const uint64_t pol = l2_policy(true);
+            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
+              p += T_s;
+            }
+          } else if (full_n) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               __stcs(p, __uint_as_float(r[j]));
@@ -834,6 +857,16 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
   return cudaSuccess;
 }
 
+// L2 policies in the GEMMs (V evict-first, M evict-last); WINO_L2_HINTS=0 disables
+static int gemm_l2hint() {
+  static int h = -1;
+  if (h < 0) {
+    const char* ev = getenv("WINO_L2_HINTS");
+    h = ev ? (atoi(ev) != 0) : 1;
+  }
+  return h;
+}
+
 template <int BN>
 static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaStream_t s, float* Mo, int P,
                              int t_lo, int T, int64_t T_s, int C, int K) {
@@ -842,15 +875,15 @@ static cudaError_t launch_bn(const TcGemm& tg, int grid, const TcSmem& sm, cudaS
   if (tg.variant == kGemmTS) {
     if (tg.resident)
       return launch_pdl(tc::k_gemm_ts<BN, true>, gd, bdts, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
-                        C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
+                        C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg, gemm_l2hint());
     return launch_pdl(tc::k_gemm_ts<BN, false>, gd, bdts, sm.bytes, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
-                      C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg);
+                      C, K, tg.kc, tg.three, sm.nraw, sm.nbr, tg.dbg, gemm_l2hint());
   }
   if (tg.resident)
     return launch_pdl(tc::k_gemm_tc<BN, true>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
-                      C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
+                      C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr, gemm_l2hint());
   return launch_pdl(tc::k_gemm_tc<BN, false>, gd, bd, sm.bytes, s, tg.tmA, tg.tmBhi, tg.tmBlo, Mo, P, t_lo, T, Ts,
-                    C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr);
+                    C, K, tg.kc, tg.three, sm.nraw, sm.nop, sm.nbr, gemm_l2hint());
 }
 
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
