@@ -238,7 +238,10 @@ cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, kern, 128, smem) != cudaSuccess ||
             grid_per_sm < 1)
           grid_per_sm = 1;
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+          sms = 148;
       }
       const int64_t nunits = ((g.T - g.t_beg + 127) / 128) * (int64_t)g.K;
       int64_t grid = (int64_t)grid_per_sm * sms;
