@@ -54,6 +54,30 @@ class Net:
             h = y
         return h
 
+    def capture(self, x, relu: bool = False):
+        """Record one forward on the device tensor `x` into a CUDA graph and
+        return a function that replays it (same x memory, result in the Net's
+        last activation).  For launch-bound small batches: one graph launch
+        replaces the 3 kernel launches per layer (measured: Figure 4 at batch
+        1, 0.106 -> 0.094 ms with F(5,4), 0.142 -> 0.107 ms with F(3,4))."""
+        import torch
+        if x.shape[0] != self.batch:
+            raise ValueError("batch %d != planned %d" % (x.shape[0], self.batch))
+        s = torch.cuda.Stream(device=x.device)
+        s.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.stream(s):
+            self.forward(x, s, relu)            # warm-up outside the capture
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self.forward(x, s, relu)
+
+        def replay():
+            graph.replay()
+            return self.acts[-1]
+        replay.graph = graph
+        return replay
+
     def close(self) -> None:
         for p in self.plans:
             p.close()

@@ -103,3 +103,20 @@ def test_chain_relu_and_batch():
 def test_chain_shape_mismatch_is_an_error():
     with pytest.raises(ValueError):
         pkg.Net([(2, (16, 16), 3, 4, 8, 8, (0, 0)), (2, (16, 16), 3, 4, 8, 8, (0, 0))], 1)
+
+
+def test_chain_graph_replay_matches_eager():
+    cfg = NETS["fig4_f34"]
+    x, gs = make_net_inputs(cfg, seed=4, batch=1)
+    net = _net(cfg, 1)
+    net.filter_transform([g.cuda() for g in gs])
+    xd = x.cuda()
+    y_eager = net.forward(xd).clone()
+    replay = net.capture(xd)
+    y_graph = replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_graph, y_eager)
+    xd.mul_(0.5)                                   # same memory, new values: the graph sees them
+    y2 = replay().clone()
+    assert torch.equal(y2, net.forward(xd))
+    net.close()
