@@ -230,7 +230,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const int nk = kc / 8;
           if (elect_one()) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+            for (int j = 0; j < 8; ++j) {  // kc <= 64: at most 8 K=8 steps
               if (j < nk) {
                 const uint32_t accum = (ch | j) != 0;
                 const uint64_t o = 64ull * j;
@@ -553,7 +553,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
           if (elect_one()) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+            for (int j = 0; j < 8; ++j) {  // kc <= 64: at most 8 K=8 steps
               if (j < nk) {
                 const uint32_t accum = (ch | j) != 0;
                 if (three) {
@@ -825,8 +825,11 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
                             int C, int K_s, int K, int three, int device) {
   tg.ready = false;
   tg.bn_max = pick_bn(K);
-  tg.kc = C >= 32 ? 32 : ((C + 7) / 8) * 8;
-  if (const char* ev = getenv("WINO_GEMM_KC")) tg.kc = atoi(ev);  // dev knob (8, 16, 32)
+  // k-chunk: 32 channels; 64 for C >= 256 (half the chunk handshakes: c4
+  // 0.789 -> 0.753 ms; at C = 128 the bigger rings leave no shared memory for
+  // the neighbouring kernels and the step gets slower, c2 0.102 -> 0.105 ms)
+  tg.kc = C >= 256 ? 64 : C >= 32 ? 32 : ((C + 7) / 8) * 8;
+  if (const char* ev = getenv("WINO_GEMM_KC")) tg.kc = atoi(ev);  // dev knob (8, 16, 32, 64)
   tg.three = three;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -852,7 +855,13 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
     const int b = atoi(ev);
     if ((b == 32 || b == 64 || b == 128) && b < bn) bn = b;
   }
-  if ((e = prep_bn(tg, bn, C)) != cudaSuccess) return e;
+  if ((e = prep_bn(tg, bn, C)) != cudaSuccess) {
+    // a 256-wide N tile does not fit the rings at this k-chunk: 128 only
+    if (bn <= 128) return e;
+    cudaGetLastError();
+    tg.bn_max = bn = 128;
+    if ((e = prep_bn(tg, bn, C)) != cudaSuccess) return e;
+  }
   tg.ready = true;
   return cudaSuccess;
 }

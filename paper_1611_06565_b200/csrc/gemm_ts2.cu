@@ -238,7 +238,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
           const uint32_t a_hi = tmem_base + a_col0 + as * 2 * kc, a_lo = a_hi + kc;
           if (elect_one()) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {  // kc <= 32: at most 4 K=8 steps
+            for (int j = 0; j < 8; ++j) {  // kc <= 64: at most 8 K=8 steps
               if (j < nk) {
                 const uint32_t accum = (ch | j) != 0;
                 if (three) {
