@@ -1,27 +1,33 @@
 // xform_in.cuh -- stage a2, the input-tile (data) transform of the N-D
 // Winograd layer on sm_100a (kernel template; instantiated by
-// xform_in_const.cu for the compile-time tables and xform_in_run.cu for
-// run-time tables):
+// xform_in_const.cu for the compile-time tables, xform_in_run(8).cu for
+// run-time tables and xform_mixed.cu for per-axis plans):
 //
-//   V_xi[c][t] = (d(b, c, t) x_1 B^T x_2 ... x_N B^T)_xi          (Eq. (4))
+//   V_xi[c][t] = (d(b, c, t) x_1 B_1^T x_2 ... x_N B_N^T)_xi        (Eq. (4))
 //
-// where d(b, c, t) is the alpha^N window of x starting at t_n*m - P_n, zero
+// where d(b, c, t) is the window of x starting at t_n*m_n - P_n, zero
 // outside the input (readings #2, #10).
 //
 // Design: the stage is HBM-bound (x read once, V written
-// once, V = (alpha/m)^N x larger than x), so one CTA owns one (b, c) plane
-// slab -- the input under tiles [a, a+bt0) of axis 0 and all tiles of the
-// other axes, which is a contiguous run of t -- and
-//   1. stages the slab into shared memory: one TMA box load whose
+// once, V = (alpha/m)^N x larger than x).  A slab is one (b, c) plane's input
+// under tiles [a, a+bt0) of axis 0 and all tiles of the other axes (a
+// contiguous run of t); a CTA owns g.npl consecutive slabs of one channel and
+//   1. stages them into shared memory: one TMA box load per slab whose
 //      out-of-bounds fill supplies the zero padding (kTma), or coalesced
-//      4-byte cp.async (fallback for shapes that break a TMA rule),
-//   2. N <= 2: one work item per tile, the whole window in registers; N >= 3:
-//      one work item per (xi_0, tile): the axis-0 combination
-//      h = sum_i B^T[xi_0][i] slab_row(i) (compile-time xi_0, so zero
-//      entries of B^T are skipped), then the remaining N-1 axes as register
-//      line transforms; window rows are read with 64/128-bit shared loads,
-//   3. writes the values V[xi][c][t]; lanes hold consecutive t, so every warp
-//      store is one coalesced 128-byte line.
+//      4-byte cp.async (fallback for shapes that break a TMA rule); each
+//      thread waits only for the slabs of its own work items,
+//   2. pools the work items of all its slabs: N <= 2: one item per tile, the
+//      whole window in registers; N = 3, alpha >= 6: the axis-0 pass in
+//      shared memory (in place for one-tile-deep slabs), then one item per
+//      (xi_0, tile), xi_0 outermost; other N >= 3: one item per (xi_0, tile)
+//      with the axis-0 combination h = sum_i B^T[xi_0][i] slab_row(i)
+//      (compile-time xi_0: zero entries skipped); r = 1 on the other axes:
+//      one item per pixel column; window rows are read with 64/128-bit
+//      shared loads,
+//   3. writes V[xi][c][t]; lanes hold consecutive t, so every warp store is
+//      one coalesced 128-byte line.
+// Axis 0's transform (alpha_0, m_0, table) is a template parameter, equal to
+// the other axes' except for per-axis plans.
 //
 // TMA requires the innermost start coordinate to be 16-byte aligned
 // (measured: a start of -1 float faults, -4 works), so the TMA slab starts

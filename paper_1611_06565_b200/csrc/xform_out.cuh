@@ -1,6 +1,8 @@
 // xform_out.cuh -- stage a4, the output transform + scatter of the N-D
-// Winograd layer (kernel template; instantiated by xform_out_const.cu and
-// xform_out_run.cu):
+// Winograd layer (kernel template; instantiated by xform_out_const.cu,
+// xform_out_run.cu and xform_mixed.cu): a plain kernel with per-thread loads
+// of M, and a TMA-ring kernel for alpha^(N-1) >= 32 (k_output_xform_tma);
+// axis 0's transform is a template parameter (per-axis plans):
 //
 //   y tile(b, k, t) = M[.][k][t] x_1 A^T ... x_N A^T, cropped to `out`
 // (Eq. (4); stitching of overlapping tiles PAPER.md:221).
