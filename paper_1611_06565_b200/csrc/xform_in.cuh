@@ -273,31 +273,40 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int tl1 = g.tiles[1], tl2 = g.tiles[2];
     if (g.hinplace) {
-      // bt0 = 1: phase 1 rewrites every slab column (y, x) in place with its
-      // alpha axis-0 outputs (the column is private to its thread; lanes =
-      // consecutive x, conflict-free)
+      // bt0 = 1: phase 1 rewrites every slab column (y, x) with its alpha
+      // axis-0 outputs, shifted D columns left (column x + D -> x) so that
+      // the phase-2 window rows are 16-byte aligned (128/64-bit loads, fewer
+      // bank conflicts).  A row belongs to one warp and is walked in
+      // increasing x, and within a warp every lane's loads precede the
+      // stores, so each source value is read before its slot is overwritten
+      // (lanes = consecutive x, conflict-free)
       for (int r = warp; r < npl * e1; r += nwarps) {
         const int p = r / e1, y = r - p * e1;
         ensure(p);
-        float* row = S0 + p * slab_f + y * g.sst[1] + D;
-        for (int xh = lane; xh < e2; xh += 32) {
-          float* col = row + xh;
+        float* row = S0 + p * slab_f + y * g.sst[1];
+        for (int xb = 0; xb < e2; xb += 32) {  // every lane runs every pass (warp-wide sync below)
+          const int xh = xb + lane;
+          const bool act = xh < e2;
           float v[A0];
 #pragma unroll
-          for (int i = 0; i < A0; ++i) v[i] = col[i * g.sst[0]];
+          for (int i = 0; i < A0; ++i) v[i] = act ? row[xh + D + i * g.sst[0]] : 0.f;
+          __syncwarp();  // all reads of this pass before any shifted write
+          if (act) {
 #pragma unroll
-          for (int x0 = 0; x0 < A0; ++x0) {
-            float acc = 0.f;
-            bool first = true;
+            for (int x0 = 0; x0 < A0; ++x0) {
+              float acc = 0.f;
+              bool first = true;
 #pragma unroll
-            for (int i = 0; i < A0; ++i) {
-              if (Get0::nz(xp, x0, i)) {
-                acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
-                first = false;
+              for (int i = 0; i < A0; ++i) {
+                if (Get0::nz(xp, x0, i)) {
+                  acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
+                  first = false;
+                }
               }
+              row[xh + x0 * g.sst[0]] = acc;
             }
-            col[x0 * g.sst[0]] = acc;
           }
+          __syncwarp();  // writes of this pass before the next pass's reads
         }
       }
       __syncthreads();
@@ -315,7 +324,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
         float h[A * A];
 #pragma unroll
-        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, D>(hp0 + i1 * g.sst[1], h + i1 * A);
+        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, 0>(hp0 + i1 * g.sst[1], h + i1 * A);
         all_axes<A, 2, A, A, Get>(h, xp);
         float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
