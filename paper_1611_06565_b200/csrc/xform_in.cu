@@ -71,13 +71,16 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
 // of one channel (adjacent runs of t in V) and pools their work items, xi_0
 // outermost in H mode, so each round of the block stores long runs of t per
 // plane of V.  Measured (B200, tools/in_sweep.sh): c2 37.1 -> 32.8 us and c4
-// 0.297 -> 0.247 ms at npl = 2, both worse at 3 and 4 -> two slabs per CTA
-// when they fit 64 KB, keeping >= 4 CTAs per SM of work.  Not with a
-// separate H buffer.
+// 0.297 -> 0.247 ms at npl = 2 -> two slabs per CTA when they fit 64 KB,
+// keeping >= 4 CTAs per SM of work; in-place H mode (aligned rows) four.
+// Not with a separate H buffer.
 void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
   const bool pooled = g.hinplace || g.hpitch == 0;
   int npl = 1;
   if (pooled && 2 * g.slot_bytes <= 64 * 1024 && nwork / 2 >= 4LL * num_sms) npl = 2;
+  // H mode in place (aligned phase-2 rows): four one-tile-deep slabs per CTA
+  // when they fit ~104 KB (c4 input 0.237 -> 0.218 ms at npl 4 vs 2)
+  if (g.hinplace && 4 * g.slot_bytes <= 104 * 1024 && nwork / 4 >= 2LL * num_sms) npl = 4;
   if (const char* ev = getenv("WINO_IN_NPL")) npl = atoi(ev);  // dev knob
   if (npl < 1) npl = 1;
   if (npl > kMaxPlanes) npl = kMaxPlanes;
