@@ -80,7 +80,8 @@ void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
   if (pooled && 2 * g.slot_bytes <= 64 * 1024 && nwork / 2 >= 4LL * num_sms) npl = 2;
   // H mode in place (aligned phase-2 rows): four one-tile-deep slabs per CTA
   // when they fit ~104 KB (c4 input 0.237 -> 0.218 ms at npl 4 vs 2)
-  if (g.hinplace && 4 * g.slot_bytes <= 104 * 1024 && nwork / 4 >= 2LL * num_sms) npl = 4;
+  // (deep slabs only: a single-plane slab -- F(1,1) along axis 0 -- keeps 2)
+  if (g.hinplace && g.e[0] >= 4 && 4 * g.slot_bytes <= 104 * 1024 && nwork / 4 >= 2LL * num_sms) npl = 4;
   if (const char* ev = getenv("WINO_IN_NPL")) npl = atoi(ev);  // dev knob
   if (npl < 1) npl = 1;
   if (npl > kMaxPlanes) npl = kMaxPlanes;

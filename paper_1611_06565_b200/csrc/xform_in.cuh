@@ -280,6 +280,9 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // increasing x, and within a warp every lane's loads precede the
       // stores, so each source value is read before its slot is overwritten
       // (lanes = consecutive x, conflict-free)
+      // (alpha_0 = 1, F(1,1): the axis-0 pass is the identity and is skipped;
+      // phase 2 then reads the slab rows at their D offset)
+      if constexpr (A0 > 1) {
       for (int r = warp; r < npl * e1; r += nwarps) {
         const int p = r / e1, y = r - p * e1;
         ensure(p);
@@ -309,6 +312,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           __syncwarp();  // writes of this pass before the next pass's reads
         }
       }
+      }
       __syncthreads();
       // phase 2: one work item per (xi_0, plane, t1, t2) on plane xi_0 of its
       // slab; xi_0 outermost, so a round of the block writes long runs of t
@@ -323,8 +327,10 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         const int t1 = tl / tl2, t2 = tl - t1 * tl2;
         const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
         float h[A * A];
+        if constexpr (A0 == 1) ensure(p);
+        constexpr int DS = A0 > 1 ? 0 : D;  // shifted by phase 1, else at the TMA offset
 #pragma unroll
-        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, 0>(hp0 + i1 * g.sst[1], h + i1 * A);
+        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
         all_axes<A, 2, A, A, Get>(h, xp);
         float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
