@@ -113,9 +113,11 @@ WINO_API wino_status wino_plan_create_ex(wino_plan_t* plan, int N, const int64_t
  * along space, or anisotropic kernels r = (1,3,3).  m[0..N), r[0..N) >= 1
  * with alpha_n = m_n + r_n - 1 <= 8 and prod alpha_n <= 65535; default
  * points per alpha_n; g is [K][C][r_1]..[r_N].  Equal (m_n, r_n) on every
- * axis returns the plan of wino_plan_create_ex (fused kernels); otherwise the
- * plan runs generic multi-pass transforms around the same GEMM (no fusion
- * bitmask).  Errors as wino_plan_create_ex. */
+ * axis returns the plan of wino_plan_create_ex (fused kernels); N = 2, 3 with
+ * a distinct axis 0 over equal other axes, each of F(2,3), F(4,3), F(1,1),
+ * runs fused kernels with an axis-0 transform of its own (info axis_mode 1);
+ * any other mix runs generic multi-pass transforms around the same GEMM
+ * (axis_mode 2).  No fusion bitmask.  Errors as wino_plan_create_ex. */
 WINO_API wino_status wino_plan_create_nd(wino_plan_t* plan, int N, const int64_t* dims, const int* m,
                                          const int* r, int C, int K, int batch, const int* padding,
                                          int gemm_mode, int device);
