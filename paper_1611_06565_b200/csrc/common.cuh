@@ -60,7 +60,7 @@ struct KGeom {
   int hpitch;                // N = 3, alpha >= 6: row pitch of the axis-0 pass buffer H
   int hinplace;              // N = 3, alpha >= 6, bt0 = 1: the axis-0 pass overwrites the slab (no H)
   int npl;                   // slabs per CTA (consecutive work items, one TMA box each)
-  int in_threads;            // block size of the input kernel (<= 256)
+  int in_threads;            // block size of the input kernel (<= 256; <= 512 in H mode)
   int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
 };
 

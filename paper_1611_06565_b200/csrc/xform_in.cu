@@ -60,7 +60,7 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   g.e[0] = bt0 * m0 + halo0;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
   g.in_threads = 256;
-  if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256)
+  if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256; 512 in H mode)
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(g.slot_bytes + hb);
@@ -81,7 +81,12 @@ void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
   // H mode in place (aligned phase-2 rows): four one-tile-deep slabs per CTA
   // when they fit ~104 KB (c4 input 0.237 -> 0.218 ms at npl 4 vs 2)
   // (deep slabs only: a single-plane slab -- F(1,1) along axis 0 -- keeps 2)
-  if (g.hinplace && g.e[0] >= 4 && 4 * g.slot_bytes <= 104 * 1024 && nwork / 4 >= 2LL * num_sms) npl = 4;
+  if (g.hinplace && g.e[0] >= 4 && 4 * g.slot_bytes <= 104 * 1024 && nwork / 4 >= 2LL * num_sms) {
+    npl = 4;
+    // 384 threads for the 6 x 196 pooled items of a c4 CTA (measured: input
+    // 0.216 -> 0.206 ms vs 256, 0.209 at 512)
+    if (!getenv("WINO_IN_THREADS")) g.in_threads = 384;
+  }
   if (const char* ev = getenv("WINO_IN_NPL")) npl = atoi(ev);  // dev knob
   if (npl < 1) npl = 1;
   if (npl > kMaxPlanes) npl = kMaxPlanes;

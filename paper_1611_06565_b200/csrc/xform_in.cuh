@@ -479,8 +479,15 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
 // the same channel).  kTma (N >= 2): each slab is one TMA box starting D
 // columns left of -P_last, all npl boxes issued at once; !kTma: cp.async
 // fallback, D == 0.
+// Block-size bound: 512 for the N = 3, alpha >= 6 (H mode) instantiations,
+// whose four-slab CTAs run 384 threads (plan_input_planes); 256 elsewhere,
+// which keeps the other instantiations at <= 48 registers (measured: the
+// 512 bound raises them to 64 and costs c2 32.7 -> 34.5 us).
+template <int N, int A>
+constexpr int in_max_threads() { return (N == 3 && A >= 6) ? 512 : 256; }
+
 template <int N, int A, int M, class Tab, int D, bool kTma, class Ax = Ax0<A, M, Tab>>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(in_max_threads<N, A>())
 k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_constant__ KGeom g,
               const __grid_constant__ XfParams xp, const __grid_constant__ CUtensorMap tm, int nslab) {
   extern __shared__ __align__(128) float smem_f[];
