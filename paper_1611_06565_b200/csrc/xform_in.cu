@@ -60,7 +60,11 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   g.e[0] = bt0 * m0 + halo0;
   if (N == 1) g.pitch = (g.e[0] + 3) / 4 * 4;
   g.in_threads = 256;
-  if (const char* ev = getenv("WINO_IN_THREADS")) g.in_threads = atoi(ev);  // dev knob (64..256; 512 in H mode)
+  if (const char* ev = getenv("WINO_IN_THREADS")) {  // dev knob, clamped to the kernel's launch bound
+    const int tmax = hmode ? 512 : 256;               // (in_max_threads: 512 in H mode, else 256)
+    g.in_threads = (atoi(ev) + 31) / 32 * 32;
+    g.in_threads = g.in_threads < 64 ? 64 : g.in_threads > tmax ? tmax : g.in_threads;
+  }
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(g.slot_bytes + hb);
