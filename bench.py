@@ -2,23 +2,29 @@
 """bench.py -- N-D Winograd conv layer F(m^N, r^N) on B200 (arXiv 1611.06565).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2] [--extra c3,c4,c5] [--scaling weak|strong]
+                    [--config c4] [--extra c2,c3,c5,c1] [--scaling strong|weak]
 
 Metric (BASELINE.json): direct-convolution-equivalent TFLOP/s and ms per layer.
 A step is one full forward of the layer (stages a2 input transform -> a3
 per-point GEMM -> a4 output transform) over one batch that is already
 resident in HBM; the filter transform a1 runs once per weight set (the
 paper caches transformed kernels) and is reported separately.
-The headline workload is BASELINE.json configs[1] (c2); the other configs
-are reported under "configs".  L2 is flushed between timed steps, outside
-the per-step CUDA events: a 256 MiB memset followed by a 256 MiB read, so the
-dirty lines of the memset are written back before the step starts (cold,
-clean L2; WINO_BENCH_DIRTY_FLUSH=1 keeps the memset only).
+The headline workload is c4 (BASELINE.json configs[3], the largest
+single-GPU config by direct-equivalent work: the paper's 6x6x6 C3D example,
+PAPER.md:191-219); c1, c2, c3 and c5 are reported under "configs".  L2 is
+flushed between timed steps, outside the per-step CUDA events: a 256 MiB
+memset followed by a 256 MiB read, so the dirty lines of the memset are
+written back before the step starts (cold, clean L2;
+WINO_BENCH_DIRTY_FLUSH=1 keeps the memset only).
 
-Multi-GPU (torchrun, one process per GPU, NCCL): the batch shards with no
-per-forward collective; rank 0 transforms the filters and broadcasts U once
-(SURVEY.md 8(e)).  "weak" (default): every rank convolves a full config-size
-batch; "strong": the config batch is split.  Time = max over ranks.
+Multi-GPU: one process per GPU over NCCL.  `--gpus N` without a torchrun
+environment re-launches this script under `torch.distributed.run` with N
+ranks (127.0.0.1 rendezvous).  The batch shards with no per-forward
+collective; rank 0 transforms the filters and broadcasts U once (SURVEY.md
+8(e)).  "strong" (default): the config batch is split over the ranks (a
+(batch x K) grid when the batch is smaller than N); "weak": every rank
+convolves a full config-size batch (also reported for the headline config
+when N > 1).  Time = max over ranks of device-event time.
 
 --impl reference times the CPU float64 oracle (oracle/, the only reference
 that exists for this paper) on a bounded sample of the same workload.
@@ -42,6 +48,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "direct-equiv TFLOP/s and ms per N-D Winograd conv layer at 1/2/4/8 B200"
 GUIDE_TF32_OVER_BF16 = 1.1 / 2.25          # B200_PROFILING.md nominal dense ratio
+PARITY_SAMPLES = 4096                       # random outputs per config in the bench's parity block
 
 
 def parse_args():
@@ -50,9 +57,12 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
-    ap.add_argument("--extra", default="c3,c4,c5", help="comma list of further configs ('' for none)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--extra", default="c2,c3,c5,c1", help="comma list of further configs ('' for none)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the ranks, agree on the world size, print one JSON line, exit (no GPU work)")
+    ap.add_argument("--no-tf32-peak", action="store_true", help="skip the on-box cuBLAS TF32 peak measurement")
     ap.add_argument("--fuse", type=int, default=0, help="plan fuse bitmask (4 = L2-chunked a2->a3->a4)")
     ap.add_argument("--nets", default="fig4_f54,fig4_f34,fig3_f54",
                     help="the paper's own 2-D workloads (Figures 3 and 4) to time at N=1 ('' for none)")
@@ -133,23 +143,80 @@ def stage_bytes(cfg, B):
     return {s: st[s]["bytes"] for s in ("input_xform", "gemm", "output_xform")}
 
 
+def tf32_peak(peaks):
+    """TF32 dense peak (TFLOP/s) for the per-point GEMM's roofline: the larger
+    (more conservative) of the on-box cuBLAS TF32 measurement and the measured
+    bf16 peak x the guide's nominal TF32/bf16 ratio."""
+    nominal = peaks["bf16"] * GUIDE_TF32_OVER_BF16
+    return max(nominal, peaks.get("tf32_measured") or 0.0)
+
+
+def gemm_tensor_util(cfg, B, ms, peaks):
+    """Tensor-pipe utilisation of the per-point GEMM: 3 TF32 products per fp32
+    multiply-add (3xTF32), 3 * 2 alpha^N T C K / (t * TF32 peak)."""
+    return 3 * cfg.winograd_gemm_flops(B) / (ms * 1e-3) / 1e12 / tf32_peak(peaks)
+
+
 def roofline_for(cfg, B, stage, ms, peaks):
     t = ms * 1e-3
     nbytes = stage_bytes(cfg, B)[stage]
-    tf32 = peaks["bf16"] * GUIDE_TF32_OVER_BF16
+    tf32 = tf32_peak(peaks)
     if stage == "gemm":
         flops = cfg.winograd_gemm_flops(B)
         t_mem = nbytes / (peaks["hbm_gbs"] * 1e9)
         t_tc = flops / (tf32 / 3 * 1e12)
+        util = round(gemm_tensor_util(cfg, B, ms, peaks), 4)
         if t_tc > t_mem:
             ach = flops / t / 1e12
             return {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32 / 3, 1), "unit": "TFLOP/s",
-                    "frac": round(ach / (tf32 / 3), 4), "traffic": None,
-                    "note": "fp32 flops of the per-point GEMM vs 3xTF32 fp32-equivalent peak = "
-                            "(bf16 %s x 1.1/2.25) / 3" % peaks["source"]}
+                    "frac": round(ach / (tf32 / 3), 4), "traffic": None, "tensor_util": util,
+                    "note": "fp32 flops of the per-point GEMM vs the 3xTF32 fp32-equivalent peak = TF32 peak / 3; "
+                            "TF32 peak = max(on-box cuBLAS TF32, bf16 %s x 1.1/2.25)" % peaks["source"]}
+        ach = nbytes / t / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "tensor_util": util}
     ach = nbytes / t / 1e9
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None}
+
+
+def measure_tf32_peak(dev):
+    """cuBLAS fp32 matmul with TF32 tensor cores, 8192^3, best of 10 (CUDA
+    events): the on-box TF32 dense peak."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        c = torch.empty(n, n, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b, c
+        torch.cuda.empty_cache()
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def load_traffic():
@@ -158,7 +225,24 @@ def load_traffic():
 
 
 # ------------------------------------------------------------------ ours
-def run_ours(args, cfg_names, rank, world, local, peaks):
+def layer_shard(cfg, rank, world, scaling):
+    """This rank's inputs: (x, g, B, K_local, ksplit).
+    weak: a full config batch per rank (x seeded by rank, the same g);
+    strong: the config batch over the ranks, and when the batch is smaller
+    than the world the output channels too (dist.grid_shard, NEXT-3)."""
+    from paper_1611_06565_b200 import dist as wdist
+    from paper_1611_06565_b200.workloads import make_inputs
+    if scaling == "weak":
+        x = make_inputs(cfg, seed=rank)[0]
+        g = make_inputs(cfg, seed=0)[1]              # same weights on every rank
+        return x, g, cfg.batch, cfg.K, False
+    b_lo, b_hi, k_lo, k_hi = wdist.grid_shard(cfg.batch, cfg.K, rank, world)
+    xf, gf = make_inputs(cfg, seed=0)
+    return (xf[b_lo:b_hi].contiguous(), gf[k_lo:k_hi].contiguous(), b_hi - b_lo, k_hi - k_lo,
+            k_hi - k_lo != cfg.K)
+
+
+def run_ours(args, cfg_names, rank, world, local, peaks, scaling=None):
     import torch
     import paper_1611_06565_b200 as pkg
     from paper_1611_06565_b200 import dist as wdist
@@ -178,24 +262,11 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
         if clean:
             torch.sum(flush64, dim=0, out=flush_sink)
 
+    scaling = scaling or args.scaling
     results = {}
     for name in cfg_names:
         cfg = CONFIGS[name]
-        ksplit = False
-        if args.scaling == "weak":
-            B, Kl = cfg.batch, cfg.K
-            x, g = make_inputs(cfg, seed=rank)
-            gref = make_inputs(cfg, seed=0)[1]
-            g = gref                                  # same weights on every rank
-        else:
-            # strong: the config batch over the ranks; when the batch is
-            # smaller than the world the output channels split too (NEXT-3)
-            b_lo, b_hi, k_lo, k_hi = wdist.grid_shard(cfg.batch, cfg.K, rank, world)
-            B, Kl = b_hi - b_lo, k_hi - k_lo
-            ksplit = Kl != cfg.K
-            xf, g = make_inputs(cfg, seed=0)
-            x = xf[b_lo:b_hi].contiguous()
-            g = g[k_lo:k_hi].contiguous()
+        x, g, B, Kl, ksplit = layer_shard(cfg, rank, world, scaling)
         plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, Kl, B, cfg.padding, device=local, fuse=args.fuse)
         stream = torch.cuda.current_stream(dev)
         # a1 once per weight set on rank 0, U broadcast over NCCL to the
@@ -262,12 +333,26 @@ def run_ours(args, cfg_names, rank, world, local, peaks):
         torch.cuda.synchronize(dev)
         e2e_ms = wdist.max_over_ranks(sum(a.elapsed_time(b) for a, b in ee) / len(ee), device=dev)
         # whole-job flops: weak = world x one config batch; strong = one config batch
-        flops_job = world * cfg.direct_flops(B) if args.scaling == "weak" else cfg.direct_flops()
+        flops_job = world * cfg.direct_flops(B) if scaling == "weak" else cfg.direct_flops()
+        # outputs of the last forward at sampled positions (every output for
+        # small layers), for the parity block computed by the cpu_baseline leg
+        sample = None
+        if world == 1:
+            yf = yh.view(-1)
+            n_out = yf.numel()
+            if n_out <= (1 << 16):
+                idx = torch.arange(n_out)
+            else:
+                gen = torch.Generator("cpu").manual_seed(1)
+                idx = torch.cat([torch.arange(64), torch.arange(n_out - 64, n_out),
+                                 torch.randint(0, n_out, (PARITY_SAMPLES,), generator=gen)])
+            sample = (idx.numpy(), yf[idx].double().numpy())
         res = {
             "name": name, "cfg": cfg, "cfg_local": replace(cfg, K=Kl), "B": B, "ms": ms, "tflops": flops_job / (ms * 1e-3) / 1e12, "K_local": Kl,
             "stages_ms": stages, "filter_ms": filt_ms, "e2e_ms": e2e_ms,
             "e2e_tflops": flops_job / (e2e_ms * 1e-3) / 1e12,
-            "h2d": xh.numel() * 4, "d2h": yh.numel() * 4, "launches": 3 * args.steps,
+            "h2d": xh.numel() * 4, "d2h": yh.numel() * 4, "launches": plan.launches_per_forward * args.steps,
+            "sample": sample, "scaling": scaling,
             "info": plan.info,
         }
         results[name] = res
@@ -402,7 +487,7 @@ def run_nd(args, local, peaks=None):
         # per-stage roofline fractions from the cost model's compulsory bytes / flops
         from paper_1611_06565_b200.cost import stage_model
         pk = peaks or load_peaks()
-        tf32 = pk["bf16"] * GUIDE_TF32_OVER_BF16
+        tf32 = tf32_peak(pk)
         sm = stage_model(w["N"], w["dims"], w["m"], w["r"], w["C"], w["K"], w["B"], w["pad"],
                          hbm_gbs=pk["hbm_gbs"], tf32_tflops=tf32)
         frac = {}
@@ -425,30 +510,54 @@ def run_nd(args, local, peaks=None):
     return out
 
 
-def cpu_baseline_sample(cfg, seconds):
-    """Time the float64 oracle (as it stands) on a bounded sample of the
-    workload: outputs computed one by one at random positions."""
+def cpu_baseline_leg(results, head, seconds):
+    """The cpu_baseline leg: the float64 oracle (as it stands, OpenMP on the
+    host cores) evaluated one output at a time at the positions bench.py kept
+    from each config's last end-to-end forward.  Its timing on the headline
+    config (extended to a bounded sample of about `seconds` of CPU work) is
+    the reported CPU baseline; the same oracle values give the parity block
+    (relL2 and max-abs / max|y| over the sampled outputs, in float64;
+    full-size element-wise checks are in tests/test_gpu_parity.py)."""
     import numpy as np
     from oracle import direct
-    from paper_1611_06565_b200.workloads import make_inputs
-    x, g = make_inputs(cfg)
-    per_pt = 2 * cfg.C * cfg.r ** cfg.N
-    n_out = cfg.batch * cfg.K * math.prod(cfg.out_dims)
-    rng = np.random.default_rng(0)
-    xn, gn = x.numpy(), g.numpy()
-    npts = 4096
-    t0 = time.perf_counter()
-    direct.direct_conv_at(xn, gn, cfg.pad, rng.integers(0, n_out, npts))
-    dt = time.perf_counter() - t0
-    npts2 = int(min(n_out, max(npts, npts * (seconds * 0.8) / max(dt, 1e-3))))
-    idx = rng.integers(0, n_out, npts2)
-    t0 = time.perf_counter()
-    direct.direct_conv_at(xn, gn, cfg.pad, idx)
-    dt = time.perf_counter() - t0
-    return {"value": round(npts2 * per_pt / dt / 1e12, 6), "unit": "TFLOP/s", "cores": direct.num_threads(),
-            "kind": "oracle", "seconds": round(dt, 2),
-            "sample": "%d random outputs of %s (of %d), float64 direct correlation, OpenMP" % (npts2, cfg.name, n_out),
-            "ms_per_layer_extrapolated": round(cfg.direct_flops() / (npts2 * per_pt / dt) * 1e3, 1)}
+    from paper_1611_06565_b200.workloads import make_inputs, tolerance
+    parity = {}
+    cpu = None
+    for name, r in results.items():
+        if r.get("sample") is None:
+            continue
+        cfg = r["cfg"]
+        x, g = make_inputs(cfg)
+        xn, gn = x.numpy(), g.numpy()
+        idx, y_gpu = r["sample"]
+        t0 = time.perf_counter()
+        ref = direct.direct_conv_at(xn, gn, cfg.pad, idx)
+        dt = time.perf_counter() - t0
+        err = y_gpu - ref
+        rel = float(np.linalg.norm(err) / np.linalg.norm(ref))
+        mx = float(np.abs(err).max() / np.abs(ref).max())
+        tl, tm = tolerance(cfg)
+        n_out = cfg.batch * cfg.K * math.prod(cfg.out_dims)
+        parity[name] = {"F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "relL2": float("%.3e" % rel),
+                        "max_over_maxy": float("%.3e" % mx), "tol": [tl, tm], "pass": rel <= tl and mx <= tm,
+                        "outputs": "all %d" % n_out if len(idx) == n_out else
+                                   "%d sampled of %d (first/last 64 + random)" % (len(idx), n_out)}
+        if name == head:
+            per_pt = 2 * cfg.C * cfg.r ** cfg.N
+            npts = len(idx)
+            if dt < seconds * 0.5:          # extend to a bounded sample of ~`seconds` of CPU work
+                rng = np.random.default_rng(0)
+                npts = int(min(n_out, max(len(idx), len(idx) * (seconds * 0.8) / max(dt, 1e-3))))
+                more = rng.integers(0, n_out, npts)
+                t0 = time.perf_counter()
+                direct.direct_conv_at(xn, gn, cfg.pad, more)
+                dt = time.perf_counter() - t0
+            cpu = {"value": round(npts * per_pt / dt / 1e12, 6), "unit": "TFLOP/s", "cores": direct.num_threads(),
+                   "cpu_model": cpu_model(), "kind": "oracle", "seconds": round(dt, 2),
+                   "sample": "%d random outputs of %s (of %d), float64 direct correlation, OpenMP"
+                             % (npts, cfg.name, n_out),
+                   "ms_per_layer_extrapolated": round(cfg.direct_flops() / (npts * per_pt / dt) * 1e3, 1)}
+    return cpu, parity
 
 
 def cfg_dict(cfg, B, world, scaling, fuse=0):
@@ -470,30 +579,88 @@ def cfg_dict(cfg, B, world, scaling, fuse=0):
                   else "flushed: 256 MiB memset between timed steps, outside the per-step events"}
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_under_torchrun(n):
+    """`--gpus N` without a torchrun environment: re-run this script with N
+    ranks, one per GPU, under torch.distributed.run (127.0.0.1 rendezvous)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "8")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world, local):
+    """Start the process group, agree on the world size, print one line."""
+    import torch
+    import torch.distributed as dist
+    use_nccl = torch.cuda.is_available() and torch.cuda.device_count() > local
+    if world > 1:
+        if use_nccl:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        got = [None] * world
+        dist.all_gather_object(got, {"rank": rank, "world": world, "gpus_arg": args.gpus})
+        dist.destroy_process_group()
+    else:
+        got = [{"rank": 0, "world": 1, "gpus_arg": args.gpus}]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "backend": ("nccl" if use_nccl else "gloo")
+                          if world > 1 else None, "ranks": got}))
+    return 0
+
+
 def main():
     args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch_under_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d (launch with --nproc-per-node %d, or drop "
+                         "the torchrun environment)" % (args.gpus, world, args.gpus))
     from paper_1611_06565_b200.workloads import CONFIGS
 
     if args.impl == "reference":
         if rank != 0:
             return 0
         return run_reference(args, world)
+    if args.dry_run:
+        return dry_run(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's INIT log (to stderr: stdout carries the JSON line) shows the
+        # communicator's nranks / transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
+    if not args.no_tf32_peak:
+        tf = measure_tf32_peak(torch.device("cuda", local))
+        peaks["tf32_measured"] = wdist_max(tf, world, local)
     names = [args.config] + [n for n in args.extra.split(",") if n and n != args.config]
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
     res = run_ours(args, names, rank, world, local, peaks)
     clocks = sampler.stop() if rank == 0 else None
+    weak = None
+    if world > 1 and args.scaling == "strong":
+        weak = run_ours(args, [args.config], rank, world, local, peaks, scaling="weak")[args.config]
     if world > 1:
         dist.barrier()
     if rank == 0:
@@ -515,10 +682,15 @@ def main():
             if tk is not None:
                 rl["traffic"] = tk
             # a tiny plan runs the three stages in one kernel (timed as "gemm")
-            per_stage = {s: ({"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
-                             if v > 0 else {"ms": 0.0, "note": "fused into the single-kernel tiny path"})
-                         for s, v in st.items()
-                         for rf in [roofline_for(r["cfg_local"], r["B"], s, v, peaks) if v > 0 else None]}
+            per_stage = {}
+            for sname, v in st.items():
+                if v <= 0:
+                    per_stage[sname] = {"ms": 0.0, "note": "fused into the single-kernel tiny path"}
+                    continue
+                rf = roofline_for(r["cfg_local"], r["B"], sname, v, peaks)
+                per_stage[sname] = {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
+                if sname == "gemm":
+                    per_stage[sname]["tensor_util"] = rf["tensor_util"]
             configs[name] = {"ms_per_layer": round(r["ms"], 5), "tflops_direct_equiv": round(r["tflops"], 2),
                              "stages": per_stage, "dominant": rl,
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
@@ -527,18 +699,31 @@ def main():
                                                                  "chunk_slabs", "gemm_variant", "in_slab_tiles",
                                                                  "in_planes_per_cta", "axis_mode", "tiny")}}
         out["roofline"] = configs[args.config]["dominant"]
-        out["roofline"]["peak_source"] = "of %s (MEASURED_PEAKS.json)" % peaks["source"]
+        out["roofline"]["peak_source"] = ("HBM: MEASURED_PEAKS.json (%s); tensor: TF32 = max(on-box cuBLAS "
+                                          "TF32 %s, bf16 x 1.1/2.25)" % (
+                                              peaks["source"], "%.1f TFLOP/s" % peaks["tf32_measured"]
+                                              if peaks.get("tf32_measured") else "not measured"))
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline_sample(cfg, args.cpu_seconds)
+            cpu, parity = cpu_baseline_leg(res, args.config, args.cpu_seconds)
+            out["cpu_baseline"] = cpu
+            out["parity"] = parity
         out["e2e"] = {"value": round(head["e2e_tflops"], 3), "unit": "TFLOP/s",
                       "h2d_bytes_per_step": head["h2d"], "d2h_bytes_per_step": head["d2h"],
                       "ms_per_step": round(head["e2e_ms"], 4),
                       "path": "wino_forward_host (pinned host buffers, H2D + forward + D2H + sync)"}
         out["gpu_launches"] = head["launches"]
         out["clocks"] = clocks
+        out["peaks"] = {"hbm_gbs": peaks["hbm_gbs"], "bf16_tflops": peaks["bf16"],
+                        "tf32_tflops_measured": None if not peaks.get("tf32_measured")
+                        else round(peaks["tf32_measured"], 1),
+                        "tf32_tflops_used": round(tf32_peak(peaks), 1)}
         out["filter_transform_ms"] = configs[args.config]["filter_transform_ms"]
         out["stages"] = configs[args.config]["stages"]
         out["configs"] = configs
+        if weak is not None:
+            out["weak_scaling"] = {"config": args.config, "per_gpu_batch": weak["B"],
+                                   "global_batch": weak["B"] * world, "ms_per_layer": round(weak["ms"], 5),
+                                   "value": round(weak["tflops"], 3), "unit": "TFLOP/s"}
         if world == 1 and args.nets:
             out["paper_workloads"] = run_nets(args, local)
         if world == 1 and args.nd:
@@ -547,6 +732,14 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def wdist_max(v, world, local):
+    if world == 1:
+        return v
+    from paper_1611_06565_b200 import dist as wdist
+    import torch
+    return wdist.max_over_ranks(v, device=torch.device("cuda", local))
 
 
 def run_reference(args, world):

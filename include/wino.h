@@ -87,7 +87,18 @@ enum {
  * the default points of alpha (reading #5), check the Eq. (1)
  * identity exactly (else WINO_ERR_SYNTH), upload fp32/fp64 constants, and
  * allocate the transformed-filter buffer U and the workspace (V, M) for up
- * to `batch` samples on the current device.  No kernel is launched.
+ * to `batch` samples on the current device.
+ * Device work at plan creation (none of it on the caller's streams): the
+ * workspace is zeroed, and the tcgen05 GEMM variant / N tile are chosen by
+ * timing the supported candidates on the plan's own workspace (about 4 rounds
+ * x up to 6 candidates x 3 GEMM launches, milliseconds).  Both run on a
+ * private non-blocking stream that is synchronised before returning (the
+ * device and other streams are not), and the timing choice is cached per
+ * (device, shape) in the process, so a second plan of the same shape
+ * launches no timing kernels.  The choice never changes results: every
+ * variant computes bit-identical outputs (tests/test_gpu_parity.py).  The
+ * environment variable WINO_GEMM_VARIANT=0/1/2 fixes the variant without
+ * timing.
  *   N        number of spatial dims, 1..4
  *   dims     N input extents in_n >= 1
  *   m, r     output-tile length S and kernel length G of F(m, r)
@@ -160,13 +171,14 @@ WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, fl
 WINO_API wino_status wino_plan_out_dims(wino_plan_t plan, int64_t* out);
 /* Device bytes: workspace (V + M) and filter buffer (U_hi + U_lo). */
 WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, size_t* filter_bytes);
-/* info[0..21): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
+/* info[0..22): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
  * (alpha^N), K_stride, gemm_mode, fuse, n_blk, k_chunk, chunk_slabs (0 =
  * unchunked), gemm_variant (0 SMEM-A, 1 TMEM-A, 2 CTA-pair; -1 FFMA; chosen by
  * timing the supported variants once in plan_create), input slab depth bt0,
  * input slabs per CTA npl, axis mode (0 one F(m, r) on every axis, 1 fused
  * kernels with a distinct axis-0 F(m0, r0), 2 generic per-axis passes), tiny
- * (1: the whole forward runs in one kernel, chosen for tiny layers). */
+ * (1: the whole forward runs in one kernel, chosen for tiny layers), launches
+ * (kernel launches of one full-batch forward). */
 WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
 
 /* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------

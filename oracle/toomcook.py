@@ -266,12 +266,3 @@ def sparsity(Mx) -> float:
     """Fraction of exactly-zero entries (Table 1)."""
     flat = [v for row in Mx for v in row]
     return sum(1 for v in flat if v == 0) / len(flat)
-
-
-def theoretical_speedup(S: int, Gk: int, N: int) -> float:
-    """(S G / D)^N."""
-    return (S * Gk / (S + Gk - 1)) ** N
-
-
-def frac_str(f: Fraction) -> str:
-    return str(f.numerator) if f.denominator == 1 else "%d/%d" % (f.numerator, f.denominator)

@@ -61,18 +61,28 @@ def tile_geometry(in_dims, r, m, pad):
 
 
 def extract_tiles(x: np.ndarray, m, alpha, pad, zero):
-    """x [B][C][in...] -> tiles [B][C][t_1..t_N][alpha_1..alpha_N], zero-filled."""
+    """x [B][C][in...] -> tiles [B][C][t_1..t_N][alpha_1..alpha_N], zero-filled:
+    tile t, window position w reads x at t_n m_n - P_n + w_n (zero outside
+    [0, in_n)), readings #2, #10.  Written as: zero-extend x by P_n before and
+    as far as the last window reaches after, then for every window position w
+    take the strided slice w_n, w_n + m_n, ... along each axis."""
     N = x.ndim - 2
     m, alpha = _per_axis(m, N), _per_axis(alpha, N)
     r = tuple(a - mn + 1 for a, mn in zip(alpha, m))
     out, tiles = tile_geometry(x.shape[2:], r, m, pad)
+    span = tuple(tiles[n] * m[n] + alpha[n] - m[n] for n in range(N))     # padded extent the tiles read
+    xp = np.empty(x.shape[:2] + span, dtype=x.dtype)
+    xp[...] = zero
+    src, dst = [], []
+    for n in range(N):
+        lo, hi = pad[n], min(span[n], pad[n] + x.shape[2 + n])             # x index i lands at i + P_n
+        dst.append(slice(lo, hi))
+        src.append(slice(0, hi - lo))
+    xp[(slice(None), slice(None)) + tuple(dst)] = x[(slice(None), slice(None)) + tuple(src)]
     res = np.empty(x.shape[:2] + tiles + alpha, dtype=x.dtype)
-    res[...] = zero
-    for tidx in np.ndindex(*tiles):
-        for w in np.ndindex(*alpha):
-            src = tuple(tidx[n] * m[n] - pad[n] + w[n] for n in range(N))
-            if all(0 <= src[n] < x.shape[2 + n] for n in range(N)):
-                res[(slice(None), slice(None)) + tidx + w] = x[(slice(None), slice(None)) + src]
+    for w in np.ndindex(*alpha):
+        sl = tuple(slice(w[n], w[n] + m[n] * tiles[n], m[n]) for n in range(N))
+        res[(slice(None), slice(None)) + tuple(slice(None) for _ in range(N)) + w] = xp[(slice(None), slice(None)) + sl]
     return res, out, tiles
 
 
@@ -135,13 +145,10 @@ def winograd_nd(x, g, pad, A, B, C, exact: bool = False):
     for n in range(N):
         Yt = nmode_product(Yt, As[n], 2 + n)                          # [T][K][S..]
     Yt = Yt.reshape((Bn,) + tgrid + (K,) + S)
-    y = np.empty((Bn, K) + out, dtype=Dhat.dtype)
-    for b in range(Bn):
-        for tidx in np.ndindex(*tgrid):
-            for o in np.ndindex(*S):
-                dst = tuple(tidx[n] * S[n] + o[n] for n in range(N))
-                if all(dst[n] < out[n] for n in range(N)):
-                    y[(b, slice(None)) + dst] = Yt[(b,) + tidx + (slice(None),) + o]
+    # stitch: output o of tile t lands at t_n S_n + o_n; outputs past `out` are discarded
+    order = [0, 1 + N] + [a for n in range(N) for a in (1 + n, 2 + N + n)]   # [B][K][t_1][S_1]..[t_N][S_N]
+    full = Yt.transpose(order).reshape((Bn, K) + tuple(tgrid[n] * S[n] for n in range(N)))
+    y = np.ascontiguousarray(full[(slice(None), slice(None)) + tuple(slice(0, o) for o in out)])
     return y, {"U": Ghat, "V": Dhat, "Shat": Shat, "out": out, "tiles": tgrid}
 
 

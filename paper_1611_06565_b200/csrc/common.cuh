@@ -14,6 +14,7 @@ constexpr int kMaxN = 4;      // spatial dims supported on the device path
 constexpr int kMaxA = 8;      // alpha <= 8 on the device path
 constexpr int kMaxPlanes = 8;  // input-transform slabs staged per CTA
 constexpr int kMaxOutStages = 8;  // output-transform TMA ring depth
+constexpr int kMaxDevices = 64;   // per-device caches of launch attributes
 
 constexpr int ipow(int b, int e) { return e <= 0 ? 1 : b * ipow(b, e - 1); }
 
@@ -40,7 +41,7 @@ struct KGeom {
   int64_t T_s;               // row stride of V and M (multiple of 128)
   int64_t t_beg;             // first tile of this launch (output transform)
   int64_t t0;                // V / M row of tile t is t - t0 (L2-chunked buffers)
-  int64_t s_beg;             // first input slab (b * nbox0 + box) of this launch
+  int64_t s_beg;             // first input slab ((b * nbox0 + box0) * nbox1 + box1) of this launch
   int C, K;
   int m;                     // output tile length (runtime copy)
   const float* bias;         // optional per-output-channel bias b[k] of Eq. (2) (NULL = none)
@@ -50,11 +51,19 @@ struct KGeom {
   // every tile along axes 1..N-1 (a contiguous run of t), zero padded.
   int bt0;                   // tiles along axis 0 per CTA
   int nbox0;                 // ceil(tiles[0] / bt0)
-  int e[kMaxN];              // slab extents for a full box (axis 0: bt0*m + alpha - m)
+  int e[kMaxN];              // slab extents for a full box (axis 0: bt0*m + alpha - m; axis 1: bt1*m + alpha - m)
   int pitch;                 // padded last-axis extent (multiple of 4 floats)
   int dL;                    // TMA column shift of the slab rows (0 or 3)
   int sst[kMaxN];            // slab element strides (sst[N-1] = 1)
   int R;                     // tiles per axis-0 slice: prod_{n>=1} tiles[n]
+  // Axis-1 banding (N >= 3, one-tile-deep slabs whose full axis-1 extent
+  // would not fit shared memory): a slab covers tiles [a1, a1 + bt1) of axis
+  // 1 -- still one contiguous run of t, since axis 1 is the outermost axis
+  // inside an axis-0 slice.  Unbanded: bt1 = tiles[1], nbox1 = 1.
+  int bt1;                   // axis-1 tiles per slab (divides tiles[1])
+  int nbox1;                 // tiles[1] / bt1
+  int R1;                    // prod_{n>=2} tiles[n]: t stride of axis 1
+  int Rs;                    // tiles per axis-0 slice of one slab: bt1 * R1
   int slab_bytes;            // bytes of the slab (one TMA box)
   int slot_bytes;            // slab slot stride (slab_bytes rounded up to 128)
   int hpitch;                // N = 3, alpha >= 6: row pitch of the axis-0 pass buffer H

@@ -396,7 +396,11 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
   size_t smem;
   if (!ts2_smem(BN, tg.kc, &nraw, &nbr, &smem)) return cudaErrorInvalidConfiguration;
   auto kern = tc::k_gemm_ts2<BN>;
-  static size_t set_bytes = 0;
+  // per-device caches: the shared-memory opt-in is a per-context attribute
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  static size_t set_bytes_dev[kMaxDevices] = {};
+  size_t& set_bytes = set_bytes_dev[dev];
   if (set_bytes != smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -406,8 +410,10 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
   // co-resident CTA pairs: with 1 CTA / SM not every SM can host a cluster
   // member (GPC boundaries), so size the persistent grid by the occupancy
   // query, not by num_sms / 2 (a second wave of clusters doubles the time)
-  static int max_pairs = 0;
-  static size_t max_pairs_smem = 0;
+  static int max_pairs_dev[kMaxDevices] = {};
+  static size_t max_pairs_smem_dev[kMaxDevices] = {};
+  int& max_pairs = max_pairs_dev[dev];
+  size_t& max_pairs_smem = max_pairs_smem_dev[dev];
   if (max_pairs_smem != smem) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(num_sms);

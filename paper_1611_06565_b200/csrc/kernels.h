@@ -71,7 +71,9 @@ struct TcGemm {
 cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const float* Ulo, int P,
                             int64_t T_s, int C, int K_s, int K, int three, int device);
 // Time every supported variant on the plan's workspace (rows [0, T)) and keep
-// the fastest; WINO_GEMM_VARIANT=0/1/2 forces one.  Synchronises the device.
+// the fastest; WINO_GEMM_VARIANT=0/1/2 forces one.  The timing launches run
+// on a private non-blocking stream, which is synchronised (not the device);
+// results are cached per (device, shape), so re-planning launches nothing.
 // Vw: the plan's V buffer, rewritten (zeros) before each timed launch (NULL = no)
 cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K, float* Vw);
 bool ts2_supported(int bn, int kc);

@@ -163,6 +163,18 @@ struct DeviceGuard {
   }
 };
 
+// Zero device memory at plan creation on a private non-blocking stream (no
+// implicit synchronisation with the caller's streams or the legacy stream).
+cudaError_t zero_private(void* ptr, size_t bytes) {
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(ptr, 0, bytes, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return e != cudaSuccess ? e : e2;
+}
+
 constexpr int kMaxProf = 4096;
 constexpr int kHostChunks = 16;  // wino_forward_host pipeline depth
 
@@ -245,6 +257,16 @@ wino_status wino_synthesize(int m, int r, const char* points, double* AT, double
   return WINO_OK;
 }
 
+static wino_status create_generic(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
+                                  const char* points, int C, int K, int batch, const int* padding, int gemm_mode,
+                                  int device);
+
+// WINO_ND_GENERIC=1: every plan takes the generic multi-pass transforms (dev / test knob)
+static bool force_generic() {
+  const char* ev = getenv("WINO_ND_GENERIC");
+  return ev && atoi(ev) != 0;
+}
+
 // The fused-kernel plan: F(m, r) on axes 1..N-1 and F(m0, r0) on axis 0
 // (m0 = m, r0 = r for single-(m, r) plans; a distinct axis 0 only for the
 // instantiated per-axis combinations, mixed_supported()).
@@ -275,8 +297,13 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   // axis: exactly the compile-time tables of xform_mixed.cu)
   if (mixed && (points || fuse || !mixed_supported(N, a0, m0, a, m)))
     return fail(WINO_ERR_UNSUPPORTED, "no fused kernels for axis-0 F(%d,%d) with F(%d,%d) on N=%d", m0, r0, m, r, N);
-  if (a > kMaxA || a0 > kMaxA || (!mixed && !xform_supported(N, a, m, spec)))
-    return fail(WINO_ERR_UNSUPPORTED, "no device transform kernels for N=%d alpha=%d m=%d", N, a, m);
+  if (a > kMaxA || a0 > kMaxA)
+    return fail(WINO_ERR_UNSUPPORTED, "alpha = %d exceeds %d on the device path", a > a0 ? a : a0, kMaxA);
+  // single-(m, r) plans without fused kernels for (N, alpha, m) take the
+  // generic multi-pass transforms (same GEMM, same results up to rounding)
+  const int mv[kMaxN] = {m, m, m, m}, rv[kMaxN] = {r, r, r, r};
+  if (!mixed && (!xform_supported(N, a, m, spec) || force_generic()))
+    return create_generic(plan_out, N, dims, mv, rv, points, C, K, batch, padding, gemm_mode, device);
 
   wino_plan_s* p = new wino_plan_s();
   p->N = N; p->m = m; p->r = r; p->a = a; p->C = C; p->K = K; p->batch = batch;
@@ -331,12 +358,14 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   p->use_tma_in = p->use_tma_in && tma_shape;
   if (!plan_input_slab(g, N, a0, m0, a, m, p->use_tma_in)) {
     delete p;
+    // even a banded one-tile-deep slab exceeds shared memory: generic passes
+    if (!mixed) return create_generic(plan_out, N, dims, mv, rv, points, C, K, batch, padding, gemm_mode, device);
     return fail(WINO_ERR_UNSUPPORTED, "input slab of one axis-0 tile exceeds shared memory (inner extents too large)");
   }
 
   // L2 chunking: chunk_slabs input slabs per chunk, V + M of a chunk near
   // WINO_CHUNK_MB (default 48 MB, under the 126 MB L2 with x / y traffic)
-  if (fuse & WINO_FUSE_L2_CHUNK) {
+  if ((fuse & WINO_FUSE_L2_CHUNK) && g.nbox1 == 1) {  // (not with axis-1 banded slabs)
     double mb = 48.0;
     if (const char* ev = getenv("WINO_CHUNK_MB")) mb = atof(ev);
     const double slab_bytes = (double)g.bt0 * g.R * p->P * (C + K) * 4.0;
@@ -360,7 +389,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   {
     int nsm = 148;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) nsm = 148;
-    const int64_t nslab_all = p->chunked ? p->chunk_slabs : (int64_t)batch * g.nbox0;
+    const int64_t nslab_all = p->chunked ? p->chunk_slabs : (int64_t)batch * g.nbox0 * g.nbox1;
     plan_input_planes(g, nslab_all * C, nsm);
   }
   const size_t ucount = (size_t)p->P * C * p->K_s;
@@ -378,7 +407,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   }
   p->M = p->V + (size_t)p->P * C * p->T_s;
   // GEMM padding rows t in [T, T_s) of V are never written: zero them once
-  e = cudaMemset(p->V, 0, p->ws_bytes);
+  e = zero_private(p->V, p->ws_bytes);
   if (e != cudaSuccess) {
     cudaFree(p->ubuf);
     cudaFree(p->V);
@@ -449,15 +478,28 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   // the generic multi-pass path (dev / test knob)
   bool rest_equal = N >= 2;
   for (int n = 2; n < N; ++n) rest_equal = rest_equal && m[n] == m[1] && r[n] == r[1];
-  const char* ev_gen = getenv("WINO_ND_GENERIC");
-  if (rest_equal && !(ev_gen && atoi(ev_gen) != 0) && m[0] + r[0] - 1 <= kMaxA && m[1] + r[1] - 1 <= kMaxA &&
-      mixed_supported(N, m[0] + r[0] - 1, m[0], m[1] + r[1] - 1, m[1]))
-    return create_core(plan_out, N, dims, m[0], r[0], m[1], r[1], C, K, batch, padding, nullptr, gemm_mode, 0, device);
+  if (rest_equal && !force_generic() && m[0] + r[0] - 1 <= kMaxA && m[1] + r[1] - 1 <= kMaxA &&
+      mixed_supported(N, m[0] + r[0] - 1, m[0], m[1] + r[1] - 1, m[1])) {
+    wino_status st =
+        create_core(plan_out, N, dims, m[0], r[0], m[1], r[1], C, K, batch, padding, nullptr, gemm_mode, 0, device);
+    if (st != WINO_ERR_UNSUPPORTED) return st;   // (e.g. a slab too large for the fused kernels: generic)
+  }
+  return create_generic(plan_out, N, dims, m, r, nullptr, C, K, batch, padding, gemm_mode, device);
+}
+
+// The generic multi-pass per-axis plan (xform_nd.cu around the same GEMM):
+// any F(m_n, r_n) with alpha_n <= 8 per axis and any extents.  Also the
+// fallback of single-(m, r) plans the fused kernels do not cover (alpha = 7,
+// F(2,5), N = 4 with alpha > 4, slabs too large for shared memory); then
+// `points` (one list for every axis) may be given.
+static wino_status create_generic(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
+                                  const char* points, int C, int K, int batch, const int* padding, int gemm_mode,
+                                  int device) {
   Transforms tn[kMaxN];
   int64_t P = 1;
   for (int n = 0; n < N; ++n) {
     int spec;
-    wino_status st = synth_checked(m[n], r[n], nullptr, tn[n], spec);
+    wino_status st = synth_checked(m[n], r[n], points, tn[n], spec);
     if (st) return st;
     if (tn[n].a > kMaxA)
       return fail(WINO_ERR_UNSUPPORTED, "alpha_%d = m + r - 1 = %d exceeds %d on the device path", n, tn[n].a, kMaxA);
@@ -525,7 +567,7 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   cudaError_t e = cudaMalloc(&p->ubuf, p->filter_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&p->V, p->ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&p->W, (size_t)P * K * p->T_s * 4);
-  if (e == cudaSuccess) e = cudaMemset(p->V, 0, p->ws_bytes);
+  if (e == cudaSuccess) e = zero_private(p->V, p->ws_bytes);
   if (e != cudaSuccess) {
     wino_plan_destroy(p);
     cudaGetLastError();
@@ -589,11 +631,12 @@ wino_status wino_filter_transform(wino_plan_t p, const float* g, wino_stream_t s
   return WINO_OK;
 }
 
-// First tile of input slab s (flattened b * nbox0 + box).
+// First tile of input slab s (flattened (b * nbox0 + box0) * nbox1 + box1).
 static int64_t slab_tile(const KGeom& g, int64_t s) {
-  const int64_t b = s / g.nbox0, box = s % g.nbox0;
+  const int64_t s0 = s / g.nbox1, box1 = s % g.nbox1;
+  const int64_t b = s0 / g.nbox0, box = s0 % g.nbox0;
   const int64_t a0 = box * g.bt0 < g.tiles[0] ? box * g.bt0 : g.tiles[0];
-  return b * g.Tps + a0 * g.R;
+  return b * g.Tps + a0 * g.R + box1 * g.bt1 * g.R1;
 }
 
 // Stage timing (wino_profile_*): a start/end event pair around one launch.
@@ -665,7 +708,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     p->tm_x_B = B;
   }
   const CUtensorMap* tm = p->use_tma_in && p->tm_x_ok ? &p->tm_x : nullptr;
-  const int64_t nslab = (int64_t)B * g.nbox0;
+  const int64_t nslab = (int64_t)B * g.nbox0 * g.nbox1;
   const int64_t step = p->chunked ? p->chunk_slabs : nslab;
   for (int64_t s0 = 0; s0 < nslab; s0 += step) {
     const int64_t s1 = s0 + step < nslab ? s0 + step : nslab;
@@ -787,10 +830,14 @@ wino_status wino_plan_sizes(wino_plan_t p, size_t* ws, size_t* fb) {
 
 wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   if (!p || !info) return fail(WINO_ERR_ARG, "NULL argument");
-  const int64_t v[21] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  // kernel launches of one full-batch forward
+  int64_t launches = 3;
+  if (p->tiny) launches = 1;
+  else if (p->chunked) launches = 3 * (((int64_t)p->batch * p->geom.nbox0 + p->chunk_slabs - 1) / p->chunk_slabs);
+  const int64_t v[22] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
-                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0};
+                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

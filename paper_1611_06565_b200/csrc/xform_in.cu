@@ -18,35 +18,66 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   const int halo0 = alpha0 - m0;   // axis 0 (its own F(m0, r0) in per-axis plans)
   const int pl = g.pad[N - 1];
   g.dL = (tma && N >= 2) ? ((4 - pl % 4) % 4) : 0;
-  int inner = 1;  // floats of one axis-0 slab slice
   g.R = 1;
   for (int n = 1; n < N; ++n) g.R *= g.tiles[n];
-  for (int n = N - 1; n >= 1; --n) {
-    g.e[n] = g.tiles[n] * m + halo;
-    if (n == N - 1) {
-      g.pitch = (g.e[n] + g.dL + 3) / 4 * 4;
-      g.sst[n] = 1;
-      inner = g.pitch;
-    } else {
-      g.sst[n] = inner;
-      inner *= g.e[n];
-    }
-  }
-  g.sst[0] = inner;
+  g.R1 = 1;
+  for (int n = 2; n < N; ++n) g.R1 *= g.tiles[n];
+  int inner = 1;  // floats of one axis-0 slab slice
   // N = 3, alpha >= 6: H = axis-0 pass of the slab, [bt0][alpha][e1][hpitch]
   const bool hmode = N == 3 && alpha >= 6;
-  g.hpitch = hmode ? (g.e[2] + 3) / 4 * 4 : 0;
+  // slab extents of axes >= 1 for bt1 axis-1 tiles per slab
+  auto layout = [&](int bt1) {
+    g.bt1 = N >= 2 ? bt1 : 1;
+    inner = 1;
+    for (int n = N - 1; n >= 1; --n) {
+      g.e[n] = (n == 1 ? bt1 : g.tiles[n]) * m + halo;
+      if (n == N - 1) {
+        g.pitch = (g.e[n] + g.dL + 3) / 4 * 4;
+        g.sst[n] = 1;
+        inner = g.pitch;
+      } else {
+        g.sst[n] = inner;
+        inner *= g.e[n];
+      }
+    }
+    g.sst[0] = inner;
+    g.hpitch = hmode ? (g.e[2] + 3) / 4 * 4 : 0;
+  };
   auto slab = [&](int bt) {
     const int e0 = bt * m0 + halo0;
     if (N == 1) return (size_t)((e0 + 3) / 4 * 4) * 4;
     return (size_t)e0 * inner * 4;
   };
   auto hbytes = [&](int bt) { return hmode ? (size_t)bt * alpha0 * g.e[1] * g.hpitch * 4 : (size_t)0; };
+  layout(N >= 2 ? g.tiles[1] : 1);
   // one slab (+ H) near 64 KB (48 KB in H mode: measured c4 337 -> 288 us at bt0 = 1)
   int bt0 = g.tiles[0];
   size_t target = hmode ? 48 * 1024 : 64 * 1024;
   if (const char* ev = getenv("WINO_IN_TARGET_KB")) target = (size_t)atoi(ev) * 1024;  // dev knob
   while (bt0 > 1 && slab(bt0) + hbytes(bt0) > target) bt0 = (bt0 + 1) / 2;
+  // Large planes (N >= 3): when even a one-tile-deep slab is over 100 KB,
+  // band axis 1 -- the widest divisor bt1 of tiles[1] whose slab meets the
+  // target, else the widest that fits at all (C3D-size 112 x 112 planes,
+  // large volumes).  Slabs up to 100 KB stay unbanded (the
+  // measured BASELINE configs: c3 59 KB, c5 69 KB).
+  g.nbox1 = 1;
+  if (N >= 3 && bt0 == 1 && slab(1) + hbytes(1) > 100 * 1024) {
+    const int t1 = g.tiles[1];
+    int pick = 0, fit = 0;
+    for (int d = t1; d >= 1; --d) {
+      if (t1 % d) continue;
+      layout(d);
+      const size_t sz = slab(1) + (hmode ? 0 : hbytes(1));   // in-place H mode (bt0 = 1)
+      if (!fit && sz + 128 <= 200 * 1024) fit = d;
+      if (sz <= target) { pick = d; break; }
+    }
+    if (!pick) pick = fit;
+    if (!pick) pick = t1;
+    layout(pick);
+    g.nbox1 = t1 / pick;
+  }
+  g.Rs = g.bt1 * g.R1;
+  if (N < 2) g.Rs = g.R;
   // H mode with a one-tile-deep slab: every slab column is private to the
   // thread that transforms it along axis 0, so the pass writes its alpha
   // outputs back into the column (no H buffer; several slabs fit a CTA)

@@ -171,7 +171,7 @@ __device__ __forceinline__ void tma_load_slab(uint32_t dst, const CUtensorMap* t
 // Load plane (b, box, c)'s slab with cp.async (fallback path, D == 0).
 template <int N, int A, int M>
 __device__ __forceinline__ void load_slab_cpasync(float* S, const float* __restrict__ x, const KGeom& g, int b,
-                                                  int a0, int nt0, int c) {
+                                                  int a0, int nt0, int c, int o1) {
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
     const int e0 = nt0 * M + (A - M);
     const float* __restrict__ xb = x + ((int64_t)b * g.C + c) * g.in_vol;
@@ -195,7 +195,7 @@ __device__ __forceinline__ void load_slab_cpasync(float* S, const float* __restr
         const int ext = ax == 0 ? e0 : g.e[ax];
         const int i = ax == 0 ? rem : rem % ext;
         rem = ax == 0 ? 0 : rem / ext;
-        const int64_t p = (ax == 0 ? (int64_t)a0 * M : 0) - g.pad[ax] + i;
+        const int64_t p = (ax == 0 ? (int64_t)a0 * M : ax == 1 ? (int64_t)o1 : 0) - g.pad[ax] + i;
         ok = ok && p >= 0 && p < g.in[ax];
         goff += p * g.in_stride[ax];
         soff += i * g.sst[ax];
@@ -217,11 +217,11 @@ __device__ __forceinline__ void load_slab_cpasync(float* S, const float* __restr
 // Issue the TMA box of plane (b, box, c) into slab S (thread 0 only).
 template <int N, int M, int D>
 __device__ __forceinline__ void issue_slab_tma(float* S, const CUtensorMap* tm, const KGeom& g, int b, int a0, int c,
-                                               uint32_t bar) {
+                                               int o1, uint32_t bar) {
   int co[5];
   co[0] = -g.pad[N - 1] - D;
 #pragma unroll
-  for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : 0) - g.pad[ax];
+  for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : ax == 1 ? o1 : 0) - g.pad[ax];
   co[N] = b * g.C + c;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(g.slab_bytes) : "memory");
   tma_load_slab((uint32_t)__cvta_generic_to_shared(S), tm, co, bar, N + 1);
@@ -232,6 +232,7 @@ __device__ __forceinline__ void issue_slab_tma(float* S, const CUtensorMap* tm, 
 // of t per (xi, c) in V).
 struct PlaneInfo {
   int b, a0, nt0, c;
+  int a1;   // first axis-1 tile of the slab (banded slabs; 0 otherwise)
 };
 
 // Transform the CTA's npl staged planes: slab p at S0 + p * slab_f -> V rows
@@ -262,7 +263,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     }
   };
   auto vbase = [&](int p) -> float* {
-    return V + (int64_t)pl[p].c * g.T_s + ((int64_t)pl[p].b * g.Tps + (int64_t)pl[p].a0 * g.R - g.t0);
+    return V + (int64_t)pl[p].c * g.T_s +
+           ((int64_t)pl[p].b * g.Tps + (int64_t)pl[p].a0 * g.R + (int64_t)pl[p].a1 * g.R1 - g.t0);
   };
   // ---- N = 3, alpha >= 6: the axis-0 pass materialised in shared memory
   if constexpr (N == 3 && A >= 6) {
@@ -271,7 +273,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     constexpr int A0 = Ax::A, M0 = Ax::M;
     const int e1 = g.e[1], e2 = g.e[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int tl1 = g.tiles[1], tl2 = g.tiles[2];
+    const int tl1 = g.bt1, tl2 = g.tiles[2];   // slab-local tiles (axis 1 banded or whole)
     if (g.hinplace) {
       // bt0 = 1: phase 1 rewrites every slab column (y, x) with its alpha
       // axis-0 outputs, shifted D columns left (column x + D -> x) so that
@@ -393,7 +395,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     // loads, coalesced stores) and writes all alpha_0 points
     using Get0 = BTget<typename Ax::Tab>;
     constexpr int A0 = Ax::A, M0 = Ax::M;
-    const int R = g.R, nper = g.bt0 * R;
+    const int R = g.Rs, nper = g.bt0 * R;
     for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
       const int p = u / nper;
       const int w = u - p * nper;
@@ -403,8 +405,9 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       int rem = rr, off = t0l * M0 * g.sst[0];
 #pragma unroll
       for (int ax = N - 1; ax >= 1; --ax) {
-        const int ti = rem % g.tiles[ax];
-        rem /= g.tiles[ax];
+        const int ext = ax == 1 ? g.bt1 : g.tiles[ax];
+        const int ti = rem % ext;
+        rem /= ext;
         off += ti * g.sst[ax];
       }
       const float* col = S0 + p * slab_f + off + D;
@@ -434,7 +437,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     if (npl == 1) {
       // one plane: no plane index to decode (the common case for large slabs)
       ensure(0);
-      const int ntile = pl[0].nt0 * g.R;
+      const int ntile = pl[0].nt0 * g.Rs;
       float* __restrict__ vb = vbase(0);
       for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
         const int xi0 = w / ntile;
@@ -442,8 +445,9 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         int rem = tl, base = 0;
 #pragma unroll
         for (int ax = N - 1; ax >= 1; --ax) {
-          const int ti = rem % g.tiles[ax];
-          rem /= g.tiles[ax];
+          const int ext = ax == 1 ? g.bt1 : g.tiles[ax];
+          const int ti = rem % ext;
+          rem /= ext;
           base += ti * M * g.sst[ax];
         }
         base += rem * Ax::M * g.sst[0];
@@ -451,21 +455,22 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       }
       return;
     }
-    const int ntile = g.bt0 * g.R;            // tiles of a full-depth slab
+    const int ntile = g.bt0 * g.Rs;           // tiles of a full-depth slab
     const int nper = NX * ntile;
     for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
       const int p = u / nper;
       const int w = u - p * nper;
       const int xi0 = w / ntile;
       const int tl = w - xi0 * ntile;
-      if (tl >= pl[p].nt0 * g.R) continue;    // last axis-0 box of a sample is shorter
+      if (tl >= pl[p].nt0 * g.Rs) continue;   // last axis-0 box of a sample is shorter
       ensure(p);
       // local tile -> slab offset of its window
       int rem = tl, base = 0;
 #pragma unroll
       for (int ax = N - 1; ax >= 1; --ax) {
-        const int ti = rem % g.tiles[ax];
-        rem /= g.tiles[ax];
+        const int ext = ax == 1 ? g.bt1 : g.tiles[ax];
+        const int ti = rem % ext;
+        rem /= ext;
         base += ti * M * g.sst[ax];
       }
       base += rem * Ax::M * g.sst[0];
@@ -500,10 +505,12 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   const int npl = min(g.npl, nwork - w0);
   auto plane = [&](int w) {
     PlaneInfo q;
-    const int64_t slab = g.s_beg + w % nslab;
+    const int64_t slab = g.s_beg + w % nslab;    // ((b * nbox0 + box0) * nbox1 + box1)
     q.c = w / nslab;
-    q.b = (int)(slab / g.nbox0);
-    const int box = (int)(slab - (int64_t)q.b * g.nbox0);
+    const int64_t s0 = slab / g.nbox1;
+    q.a1 = (int)(slab - s0 * g.nbox1) * g.bt1;
+    q.b = (int)(s0 / g.nbox0);
+    const int box = (int)(s0 - (int64_t)q.b * g.nbox0);
     q.a0 = box * g.bt0;
     q.nt0 = min(g.bt0, g.tiles[0] - q.a0);
     return q;
@@ -519,7 +526,7 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int p = 0; p < npl; ++p) {
         const PlaneInfo q = plane(w0 + p);
-        issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, mb0 + 8u * p);
+        issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, q.a1 * M, mb0 + 8u * p);
       }
     }
     __syncthreads();
@@ -527,7 +534,8 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
     static_assert(D == 0, "the cp.async slab path is unshifted");
     __syncthreads();
     for (int p = 0; p < npl; ++p)
-      load_slab_cpasync<N, Ax::A, Ax::M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c);
+      load_slab_cpasync<N, Ax::A, Ax::M>(smem_f + p * slab_f, x, g, pl[p].b, pl[p].a0, pl[p].nt0, pl[p].c,
+                                         pl[p].a1 * M);
     __syncthreads();
   }
   transform_planes<N, A, M, Tab, D, Ax>(smem_f, slab_f, H, V, g, xp, pl, npl,

@@ -231,7 +231,12 @@ cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams
     if (tmM) {
       auto kern = k_output_xform_tma<N, A, M, Tab, Ax>;
       constexpr int smem = ns * ipow(A, N - 1) * 128 * 4;
-      static int grid_per_sm = 0, sms = 0;
+      // per-device cache: the shared-memory opt-in is a per-context attribute
+      static int grid_per_sm_dev[kMaxDevices] = {}, sms_dev[kMaxDevices] = {};
+      int dev = 0;
+      if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+      int& grid_per_sm = grid_per_sm_dev[dev];
+      int& sms = sms_dev[dev];
       if (!grid_per_sm) {
         if (smem > 46 * 1024) {
           cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -240,9 +245,7 @@ cudaError_t launch_out(const float* Mx, float* y, const KGeom& g, const XfParams
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, kern, 128, smem) != cudaSuccess ||
             grid_per_sm < 1)
           grid_per_sm = 1;
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
           sms = 148;
       }
       const int64_t nunits = ((g.T - g.t_beg + 127) / 128) * (int64_t)g.K;

@@ -213,7 +213,7 @@ def wino_plan_sizes(plan: int):
 
 INFO_KEYS = ["N", "m", "r", "alpha", "C", "K", "batch", "T_per_sample", "T_stride", "n_points", "K_stride",
              "gemm_mode", "fuse", "n_blk", "k_chunk", "chunk_slabs", "gemm_variant", "in_slab_tiles",
-             "in_planes_per_cta", "axis_mode", "tiny"]
+             "in_planes_per_cta", "axis_mode", "tiny", "launches"]
 
 
 def wino_plan_info(plan: int) -> dict:
@@ -298,15 +298,44 @@ class Plan:
         self.out_dims = wino_plan_out_dims(self.h, N)
         self.info = wino_plan_info(self.h)
 
+    @property
+    def launches_per_forward(self) -> int:
+        """Kernel launches of one full-batch forward (wino_plan_info)."""
+        return int(self.info["launches"])
+
+    # The C ABI takes raw pointers and trusts the sizes: every tensor is
+    # checked against the plan's shapes here, before its pointer is passed.
+    def _kernel_dims(self):
+        return tuple(self.r) if isinstance(self.r, tuple) else (self.r,) * self.N
+
+    def _check_x(self, x, name="x"):
+        if x.dim() != self.N + 2 or tuple(x.shape[1:]) != (self.C,) + self.dims:
+            raise ValueError("%s has shape %s, the plan needs (B, %d, %s)" %
+                             (name, tuple(x.shape), self.C, ", ".join(map(str, self.dims))))
+        if not 1 <= x.shape[0] <= self.batch:
+            raise ValueError("%s batch %d outside 1..%d (planned batch)" % (name, x.shape[0], self.batch))
+
+    def _check_y(self, y, B, name="y"):
+        want = (B, self.K) + tuple(self.out_dims)
+        if tuple(y.shape) != want:
+            raise ValueError("%s has shape %s, the plan writes %s" % (name, tuple(y.shape), want))
+
     def filter_transform(self, g, stream=None) -> None:
+        want = (self.K, self.C) + self._kernel_dims()
+        if tuple(g.shape) != want:
+            raise ValueError("g has shape %s, the plan needs %s" % (tuple(g.shape), want))
         wino_filter_transform(self.h, g, stream)
 
     def forward(self, x, y=None, stream=None, bias=None, relu=False):
         """y = conv(x) (+ bias[k]) (then ReLU): Eq. (2) with b and f optional."""
         import torch
+        self._check_x(x)
         B = x.shape[0]
         if y is None:
             y = torch.empty((B, self.K) + tuple(self.out_dims), device=x.device, dtype=torch.float32)
+        self._check_y(y, B)
+        if bias is not None and tuple(bias.shape) != (self.K,):
+            raise ValueError("bias has shape %s, the plan needs (%d,)" % (tuple(bias.shape), self.K))
         if bias is None and not relu:
             wino_forward(self.h, x, y, B, stream)
         else:
@@ -314,6 +343,8 @@ class Plan:
         return y
 
     def forward_host(self, x_host, y_host, stream=None) -> None:
+        self._check_x(x_host, "x_host")
+        self._check_y(y_host, x_host.shape[0], "y_host")
         wino_forward_host(self.h, x_host, y_host, x_host.shape[0], stream)
 
     def filter_tensor(self):

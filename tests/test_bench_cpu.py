@@ -56,3 +56,68 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["higher_is_better"] is True and d["dtype"] == "f64"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (torch.distributed.run, 127.0.0.1); both agree on WORLD_SIZE (gloo here)."""
+    env = {k: v for k, v in __import__("os").environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"], capture_output=True,
+                         text=True, timeout=300, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout                       # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["dry_run"] and d["n_gpus"] == 2
+    assert sorted(r["rank"] for r in d["ranks"]) == [0, 1]
+    assert all(r["world"] == 2 and r["gpus_arg"] == 2 for r in d["ranks"])
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(__import__("os").environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"], capture_output=True,
+                         text=True, timeout=300, cwd=str(ROOT), env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_defaults_headline_c4_strong():
+    import argparse
+    old = sys.argv
+    sys.argv = ["bench.py"]
+    try:
+        a = bench.parse_args()
+    finally:
+        sys.argv = old
+    assert a.config == "c4" and a.scaling == "strong" and a.gpus == 1
+    assert set(a.extra.split(",")) == {"c1", "c2", "c3", "c5"}
+
+
+def test_tensor_util_and_tf32_peak():
+    c4 = CONFIGS["c4"]
+    pk = dict(PEAKS, tf32_measured=900.0)
+    assert bench.tf32_peak(pk) == 900.0                                 # measured above nominal: used
+    assert bench.tf32_peak(dict(PEAKS, tf32_measured=100.0)) == pytest.approx(1600.0 * 1.1 / 2.25)
+    u = bench.gemm_tensor_util(c4, c4.batch, 0.4, pk)
+    assert u == pytest.approx(3 * c4.winograd_gemm_flops() / 0.4e-3 / 1e12 / 900.0)
+    r = bench.roofline_for(CONFIGS["c2"], 32, "gemm", 0.05, pk)
+    assert "tensor_util" in r and r["bound"] == "hbm"
+
+
+@pytest.mark.parametrize("name,world", [("c1", 4), ("c2", 2), ("c4", 8), ("c5", 8)])
+def test_strong_shards_cover_the_layer_once(name, world):
+    """--scaling strong: the ranks' (sample, kernel) shards tile the config's
+    batch x K exactly once, with the inputs the single-GPU run would see."""
+    from paper_1611_06565_b200.workloads import make_inputs
+    cfg = CONFIGS[name].with_batch(min(CONFIGS[name].batch, 8))
+    xf, gf = make_inputs(cfg)
+    cover = __import__("torch").zeros(cfg.batch, cfg.K, dtype=__import__("torch").int32)
+    for rank in range(world):
+        x, g, B, Kl, ksplit = bench.layer_shard(cfg, rank, world, "strong")
+        assert x.shape[0] == B and g.shape[0] == Kl and ksplit == (Kl != cfg.K)
+        from paper_1611_06565_b200.dist import grid_shard
+        b_lo, b_hi, k_lo, k_hi = grid_shard(cfg.batch, cfg.K, rank, world)
+        assert (x == xf[b_lo:b_hi]).all() and (g == gf[k_lo:k_hi]).all()
+        cover[b_lo:b_hi, k_lo:k_hi] += 1
+    assert (cover == 1).all()
+    xw, gw, Bw, Kw, ks = bench.layer_shard(cfg, 1, world, "weak")
+    assert Bw == cfg.batch and Kw == cfg.K and not ks and (gw == gf).all()

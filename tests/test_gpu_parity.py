@@ -174,9 +174,21 @@ def test_error_codes():
     assert ei.value.status == wino.WINO_ERR_STATE
     plan.filter_transform(g.cuda())
     x3, _ = make_inputs(cfg, batch=3)
-    with pytest.raises(pkg.WinoError) as ei:
-        plan.forward(x3.cuda())
+    y3 = torch.empty((3, cfg.K) + cfg.out_dims, device="cuda")
+    with pytest.raises(pkg.WinoError) as ei:            # the ABI's own check (B > planned batch)
+        wino.wino_forward(plan.h, x3.cuda(), y3, 3)
     assert ei.value.status == wino.WINO_ERR_ARG
+    # the binding checks every tensor shape before a pointer reaches the ABI
+    with pytest.raises(ValueError):
+        plan.forward(x3.cuda())                          # batch above the plan's
+    with pytest.raises(ValueError):
+        plan.forward(x.cuda()[:, :-1].contiguous())      # wrong channel count
+    with pytest.raises(ValueError):
+        plan.forward(x.cuda(), torch.empty((2, cfg.K + 1) + cfg.out_dims, device="cuda"))   # wrong y
+    with pytest.raises(ValueError):
+        plan.filter_transform(g.cuda()[:, :, :2].contiguous())                             # wrong g
+    with pytest.raises(ValueError):
+        plan.forward_host(x, torch.empty((2, cfg.K) + cfg.out_dims[:-1] + (1,)))
     plan.close()
 
 

@@ -1,0 +1,158 @@
+"""Pins of oracle.fp32model (the float32 error model that sets the GPU parity
+tolerances where BASELINE.json states none; reading #15).
+
+Pinned to things other than itself:
+* closed forms of the roundings (TF32 round-half-away, float32 RNE from an
+  exact rational without double rounding);
+* mode "f64" reproduces oracle.winograd's float64 algorithm, and with inputs
+  whose every intermediate is exactly representable all modes are exact
+  (equal to the direct float64 oracle);
+* the SURVEY.md Appendix B error table -- an independent float32 emulation
+  of the same configs -- is reproduced within a band, for the plain float32,
+  the sequential float32 and the 3xTF32 tensor-core model, and the 1xTF32
+  error is orders of magnitude larger (a dropped lo term would show there).
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import direct, fp32model as fm, toomcook as tc, winograd as wg
+from paper_1611_06565_b200.workloads import CONFIGS, LayerConfig, make_inputs
+
+
+def test_tf32_rna_closed_forms():
+    one = np.float32(1.0)
+    u10 = np.float32(2.0 ** -10)                     # TF32 ulp at 1
+    x = np.array([1 + 2 ** -11, 1 + 2 ** -12, 1 + 3 * 2 ** -11, -(1 + 2 ** -11), 1 + 2 ** -11 - 2 ** -23,
+                  3.0, 0.0, -0.0], dtype=np.float32)
+    h = fm.tf32_rna(x)
+    assert h[0] == one + u10                         # tie -> away from zero
+    assert h[1] == one                               # below the tie -> down
+    assert h[2] == one + 2 * u10                     # tie -> away (not to even)
+    assert h[3] == -(one + u10)
+    assert h[4] == one                               # just below the tie
+    assert h[5] == 3.0 and h[6] == 0.0
+    assert np.all(h.view(np.uint32) & 0x1FFF == 0)   # 13 low mantissa bits cleared
+    rng = np.random.default_rng(0)
+    v = (rng.standard_normal(10000) * 10.0 ** rng.integers(-6, 6, 10000)).astype(np.float32)
+    hi, lo = fm.split_tf32(v)
+    assert np.all(np.abs(v.astype(np.float64) - hi) <= 2.0 ** -11 * np.abs(v.astype(np.float64)))
+    assert np.all(np.abs(v.astype(np.float64) - hi - lo) <= 2.0 ** -22 * np.abs(v.astype(np.float64)))
+
+
+def test_f32_rne_no_double_rounding():
+    # q is just above the midpoint between 1 and 1 + 2^-23; float64 rounds it
+    # onto the midpoint and float32 would then round to even (1.0): wrong
+    q = Fraction(1) + Fraction(1, 2 ** 24) + Fraction(1, 2 ** 60)
+    assert np.float32(float(q)) == np.float32(1.0)
+    assert fm.f32_rne(q) == np.float32(1 + 2 ** -23)
+    assert fm.f32_rne(Fraction(1) + Fraction(1, 2 ** 24)) == np.float32(1.0)          # exact tie -> even
+    # tie between 1 + 2^-23 (odd mantissa) and 1 + 2^-22 (even): up to the even one
+    assert fm.f32_rne(Fraction(1) + Fraction(3, 2 ** 24)) == np.float32(1 + 2 ** -22)
+    assert fm.f32_rne(Fraction(1, 3)) == np.float32(1 / 3)
+    assert fm.f32_rne(Fraction(-5, 4)) == np.float32(-1.25)
+
+
+def test_default_points_are_distinct_and_synthesize():
+    for a in range(2, 11):
+        pts = fm.default_points(a)
+        assert len(pts) == a and len(set(pts)) == a
+        for m in range(1, a + 1):
+            ok, _ = tc.check_identity(*tc.synthesize(m, a - m + 1, pts))
+            assert ok
+
+
+@pytest.mark.parametrize("N,dims,m,r,pad", [(1, (11,), 2, 3, 1), (2, (7, 6), 4, 3, 1), (3, (4, 5, 3), 2, 3, 0),
+                                            (2, (9, 8), (2, 3), (3, 2), (1, 0))])
+def test_f64_mode_is_oracle_winograd(N, dims, m, r, pad):
+    gen = torch.Generator().manual_seed(3)
+    rs = r if isinstance(r, tuple) else (r,) * N
+    ms = m if isinstance(m, tuple) else (m,) * N
+    x = torch.randn((2, 3) + dims, generator=gen).numpy()
+    g = torch.randn((4, 3) + rs, generator=gen).numpy()
+    pads = pad if isinstance(pad, tuple) else (pad,) * N
+    y = fm.winograd_model(x, g, pads, m, r, mode="f64")
+    mats = [fm.transforms(ms[n], rs[n]) for n in range(N)]
+    yw, _ = wg.winograd_nd(x.astype(np.float64), g.astype(np.float64), pads, [M[0] for M in mats],
+                           [M[1] for M in mats], [M[2] for M in mats])
+    assert np.abs(y - yw).max() <= 1e-13 * np.abs(yw).max()
+    ref = direct.direct_conv_f64(x, g, pads)
+    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp32_seq", "3xtf32_k8", "1xtf32_k8"])
+def test_exact_when_nothing_rounds(mode):
+    # small integers, F(2,3) with {0, 1, -1, inf}: every transform entry is
+    # 0, +-1 or +-1/2 (in C; U is computed in float64) and every intermediate
+    # is an integer or half-integer far below 2^11 -- nothing rounds, even in
+    # TF32, so every model equals the float64 direct correlation exactly
+    gen = torch.Generator().manual_seed(1)
+    x = torch.randint(-3, 4, (2, 3, 7, 9), generator=gen).float().numpy()
+    g = torch.randint(-2, 3, (4, 3, 3, 3), generator=gen).float().numpy()
+    y = fm.winograd_model(x, g, 1, 2, 3, mode=mode)
+    ref = direct.direct_conv_f64(x, g, 1)
+    assert np.array_equal(y.astype(np.float64), ref)
+
+
+def _cfg1(name, **kw):
+    from dataclasses import replace
+    return replace(CONFIGS[name], batch=1, **kw)
+
+
+# SURVEY.md Appendix B (independent emulation; batch 1, seed 0, relL2 vs the
+# float64 direct result): (config, points, mode, value)
+APPENDIX_B = [
+    ("c1", None, "fp32_seq", 1.35e-7),
+    ("c2", "0,1,-1,2,-2,inf", "fp32_seq", 2.30e-6),
+    ("c2", "0,3/2,-3/2,2/3,-2/3,inf", "fp32_seq", 1.03e-6),
+    ("c4", "0,1,-1,2,-2,inf", "fp32_seq", 8.91e-6),
+    ("c4", "0,3/2,-3/2,2/3,-2/3,inf", "fp32_seq", 2.63e-6),
+    ("c5", None, "fp32_seq", 3.61e-7),
+]
+
+
+@pytest.mark.parametrize("name,points,mode,value", APPENDIX_B)
+def test_reproduces_survey_appendix_b(name, points, mode, value):
+    cfg = _cfg1(name)
+    x, g = make_inputs(cfg)
+    xn, gn = x.numpy(), g.numpy()
+    pts = tc.parse_points(points) if points else None
+    y = fm.winograd_model(xn, gn, cfg.pad, cfg.m, cfg.r, pts, mode)
+    rel, _ = fm.errors(y, direct.direct_conv_f64(xn, gn, cfg.pad))
+    print("%s %s %s relL2 %.3e (Appendix B %.2e)" % (name, points, mode, rel, value))
+    assert 0.7 * value <= rel <= 1.4 * value
+
+
+@pytest.mark.parametrize("points,value", [("0,1,-1,2,-2,inf", 4.1e-6), ("0,3/2,-3/2,2/3,-2/3,inf", 1.25e-6)])
+def test_reproduces_survey_tensor_core_model(points, value):
+    # Appendix B "tensor-core-like accumulation model": c4, a K = 64 slice,
+    # 3xTF32 with RNA hi, exact K=8 block sums, sequential RNE accumulation
+    cfg = _cfg1("c4")
+    x, g = make_inputs(cfg)
+    xn, gn = x.numpy(), g.numpy()[:64]
+    y = fm.winograd_model(xn, gn, cfg.pad, cfg.m, cfg.r, tc.parse_points(points), "3xtf32_k8")
+    rel, _ = fm.errors(y, direct.direct_conv_f64(xn, gn, cfg.pad))
+    print("c4[K=64] %s 3xtf32_k8 relL2 %.3e (Appendix B %.2e)" % (points, rel, value))
+    assert 0.7 * value <= rel <= 1.4 * value
+
+
+def test_one_tf32_product_is_far_worse():
+    # Appendix B: c2 1xTF32 3.2e-3 vs 2.3e-6 -- dropping the lo terms costs
+    # three orders of magnitude, so a model missing a term cannot pass
+    cfg = _cfg1("c2")
+    x, g = make_inputs(cfg)
+    xn, gn = x.numpy(), g.numpy()[:32]
+    ref = direct.direct_conv_f64(xn, gn, cfg.pad)
+    r1, _ = fm.errors(fm.winograd_model(xn, gn, cfg.pad, 4, 3, tc.parse_points("0,1,-1,2,-2,inf"), "1xtf32_k8"), ref)
+    r3, _ = fm.errors(fm.winograd_model(xn, gn, cfg.pad, 4, 3, tc.parse_points("0,1,-1,2,-2,inf"), "3xtf32_k8"), ref)
+    assert 1e-3 <= r1 <= 1e-2 and r3 < 1e-5 and r1 > 300 * r3
+
+
+def test_model_tolerance_shape():
+    cfg = LayerConfig("t", 2, 2, 5, 7, (13, 11), 4, 1, 5, "normal", "he")
+    x, g = make_inputs(cfg)
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), 1)
+    tl, tm, rel, mx = fm.model_tolerance(x.numpy(), g.numpy(), 1, 5, 4, ref)
+    assert tl == fm.K_REL * rel and tm == fm.K_MAX * mx and 0 < rel < 1e-4
