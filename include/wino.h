@@ -60,7 +60,7 @@ typedef enum {
   WINO_ERR_POINTS = 3,      /* point list unparsable, duplicate, >1 infinity, count != alpha */
   WINO_ERR_SYNTH = 4,       /* exact identity check failed, or rational overflow */
   WINO_ERR_STATE = 5,       /* forward before the filter transform */
-  WINO_ERR_UNSUPPORTED = 6, /* alpha or (alpha, N) not instantiated on the device path */
+  WINO_ERR_UNSUPPORTED = 6, /* alpha_n > 8, prod alpha_n > 65535, > 2^31 tiles, or an unknown fuse bit */
   WINO_ERR_CUDA = 7,        /* CUDA launch/runtime error (incl. async errors surfaced here) */
   WINO_ERR_NOMEM = 8        /* device or pinned allocation failed */
 } wino_status;
@@ -114,7 +114,14 @@ WINO_API wino_status wino_plan_create(wino_plan_t* plan, int N, const int64_t* d
  *             order, e.g. "0,3/2,-3/2,2/3,-2/3,inf" (at most one "inf").
  *   gemm_mode WINO_GEMM_* (0 = 3xTF32 on tcgen05).
  *   fuse      WINO_FUSE_* bitmask (0 = three stream-ordered kernels).
- *   device    CUDA device ordinal, -1 = current. */
+ *   device    CUDA device ordinal, -1 = current.
+ * Kernel selection: (N, alpha, m) with fused transform kernels (alpha, m in
+ * {(4,2), (4,3), (6,4), (8,5), (8,4), (8,3), (5,3), (6,3)}, N <= 3, and N = 4
+ * with alpha = 4) take them; large N >= 3 planes band the input slab along
+ * axis 1 (info in_bands).  Every other F(m, r) with alpha <= 8 -- alpha = 7,
+ * F(2,5), F(2,4), F(4,2), N = 4 with alpha > 4 -- and planes too large even
+ * for one band run the generic multi-pass transforms (info axis_mode 2;
+ * same GEMM, results equal up to rounding; `fuse` is then ignored). */
 WINO_API wino_status wino_plan_create_ex(wino_plan_t* plan, int N, const int64_t* dims, int m, int r,
                                 int C, int K, int batch, const int* padding, const char* points,
                                 int gemm_mode, int fuse, int device);
@@ -171,14 +178,16 @@ WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, fl
 WINO_API wino_status wino_plan_out_dims(wino_plan_t plan, int64_t* out);
 /* Device bytes: workspace (V + M) and filter buffer (U_hi + U_lo). */
 WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, size_t* filter_bytes);
-/* info[0..22): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
+/* info[0..23): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
  * (alpha^N), K_stride, gemm_mode, fuse, n_blk, k_chunk, chunk_slabs (0 =
  * unchunked), gemm_variant (0 SMEM-A, 1 TMEM-A, 2 CTA-pair; -1 FFMA; chosen by
  * timing the supported variants once in plan_create), input slab depth bt0,
  * input slabs per CTA npl, axis mode (0 one F(m, r) on every axis, 1 fused
  * kernels with a distinct axis-0 F(m0, r0), 2 generic per-axis passes), tiny
  * (1: the whole forward runs in one kernel, chosen for tiny layers), launches
- * (kernel launches of one full-batch forward). */
+ * (kernel launches of one full-batch forward), in_bands (axis-1 bands of the
+ * fused input transform's slab: 1 unbanded, > 1 for large N >= 3 planes, 0
+ * on the generic path). */
 WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
 
 /* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------

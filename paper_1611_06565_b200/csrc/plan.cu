@@ -834,10 +834,11 @@ wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   int64_t launches = 3;
   if (p->tiny) launches = 1;
   else if (p->chunked) launches = 3 * (((int64_t)p->batch * p->geom.nbox0 + p->chunk_slabs - 1) / p->chunk_slabs);
-  const int64_t v[22] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[23] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
-                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches};
+                         p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches,
+                         p->nd ? 0 : p->geom.nbox1};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

@@ -61,7 +61,9 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   // large volumes).  Slabs up to 100 KB stay unbanded (the
   // measured BASELINE configs: c3 59 KB, c5 69 KB).
   g.nbox1 = 1;
-  if (N >= 3 && bt0 == 1 && slab(1) + hbytes(1) > 100 * 1024) {
+  size_t band_at = 100 * 1024;
+  if (const char* ev = getenv("WINO_IN_BAND_KB")) band_at = (size_t)atoi(ev) * 1024;  // dev / test knob
+  if (N >= 3 && bt0 == 1 && slab(1) + hbytes(1) > band_at) {
     const int t1 = g.tiles[1];
     int pick = 0, fit = 0;
     for (int d = t1; d >= 1; --d) {
