@@ -697,7 +697,7 @@ def main():
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
                                                                  "chunk_slabs", "gemm_variant", "in_slab_tiles",
-                                                                 "in_planes_per_cta", "axis_mode", "tiny")}}
+                                                                 "in_planes_per_cta", "axis_mode", "tiny", "fold", "in_bands")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = ("HBM: MEASURED_PEAKS.json (%s); tensor: TF32 = max(on-box cuBLAS "
                                           "TF32 %s, bf16 x 1.1/2.25)" % (

@@ -79,6 +79,21 @@ cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, i
 bool ts2_supported(int bn, int kc);
 cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                             cudaStream_t s);
+// a3 with the output transform of the F innermost axes folded into the
+// epilogue (gemm_fold.cu): W[xo][o][k][t] = sum_q prod_f A^T[o_f][q_f] D_{xo*Q+q}
+// (Q = alpha^F points q, MO = m^F outputs o), W [P/Q * MO][K][T_s].
+constexpr int kMaxFoldQ = 64, kMaxFoldMO = 4;
+struct FoldTab {
+  float coef[kMaxFoldQ][kMaxFoldMO];   // coef[q][o], fp32 RNE of the exact product
+};
+bool fold_shape(int K, int MO, int kc, int* bn, int* g);
+bool fold_feasible(int bn, int kc, int C, int Q);   // the folded GEMM's pipeline fits TMEM / shared memory
+cudaError_t launch_gemm_fold(const TcGemm& tg, int bn, int g, int MO, float* W, int P, int Q, int64_t t_lo,
+                             int64_t T, int64_t T_s, int C, int K, const FoldTab& fold, cudaStream_t s);
+// a4 after the folded GEMM: A^T along axes 0 .. N-F-1 of W (xform_fold.cu)
+bool output_fold_supported(int N, int alpha, int m, int F, int spec);
+cudaError_t launch_output_fold(int N, int alpha, int m, int F, int spec, const float* W, float* y, const KGeom& g,
+                               const XfParams& xp, cudaStream_t s);
 // rows [t_lo, T) of every point (t_lo a multiple of 4)
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s);

@@ -221,6 +221,10 @@ struct wino_plan_s {
   int mn[kMaxN]{}, rn[kMaxN]{}, an[kMaxN]{};
   NdParams ndp{};
   float* W = nullptr;
+  // a5: output transform of the fold_F innermost axes in the GEMM epilogue
+  // (gemm_fold.cu); the M buffer then holds W [P/Q * MO][K][T_s]
+  int fold_F = 0, fold_Q = 1, fold_MO = 1, fold_bn = 0, fold_g = 0;
+  FoldTab fold_tab{};
   bool prof = false;
   int prof_calls = 0;
   std::vector<cudaEvent_t> ev;  // pool; prof_stage[i] tags pair (2i, 2i+1)
@@ -260,6 +264,48 @@ wino_status wino_synthesize(int m, int r, const char* points, double* AT, double
 static wino_status create_generic(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
                                   const char* points, int C, int K, int batch, const int* padding, int gemm_mode,
                                   int device);
+
+// a5 epilogue fusion (gemm_fold.cu): fold the output transform of the F
+// innermost axes into the GEMM.  F from WINO_FOLD (dev knob) else the
+// measured default (fold_default); kept only where the folded kernels are
+// instantiated.  coef[q][o] = prod_f A^T[o_f][q_f], exact then RNE to fp32.
+static int fold_default(const wino_plan_s* p) {
+  // F(2^N, 3^N) with the default points, F = 2 (tools/fold_bench.sh, B200,
+  // ms per layer): c5 (N = 4) 0.192 -> 0.158 (GEMM 0.092 -> 0.085, a4 0.052 ->
+  // 0.019); c3 (N = 3) 1.700 -> 1.655 (GEMM 0.84 -> 1.17, a4 0.54 -> 0.19).
+  // Not F = 1 on c3 (1.73: the 64-wide N tile doubles the conversions) nor
+  // F(4^2, 3^2) (c2 0.100 -> 0.155: 128 channels through a 32-wide tile)
+  if (p->a == 4 && p->m == 2 && p->N >= 3) return 2;
+  return 0;
+}
+
+static void plan_fold(wino_plan_s* p) {
+  int F = fold_default(p);
+  if (const char* ev = getenv("WINO_FOLD")) F = atoi(ev);
+  if (F < 1 || F >= p->N) return;
+  const int a = p->a, m = p->m;
+  const int Q = ipow(a, F), MO = ipow(m, F);
+  if (Q > kMaxFoldQ || MO > kMaxFoldMO || !output_fold_supported(p->N, a, m, F, p->spec)) return;
+  int bn = 0, g = 0;
+  if (!fold_shape(p->K, MO, p->tg.kc, &bn, &g) || !fold_feasible(bn, p->tg.kc, p->C, Q)) return;
+  for (int q = 0; q < Q; ++q)
+    for (int o = 0; o < MO; ++o) {
+      RatOps ro;
+      Rat c{1, 1};
+      int qq = q, oo = o;
+      for (int f = 0; f < F; ++f) {   // digits, last axis fastest
+        c = ro.mul(c, p->tf.AT[oo % m][qq % a]);
+        qq /= a;
+        oo /= m;
+      }
+      p->fold_tab.coef[q][o] = rat_to_f32(c);
+    }
+  p->fold_F = F;
+  p->fold_Q = Q;
+  p->fold_MO = MO;
+  p->fold_bn = bn;
+  p->fold_g = g;
+}
 
 // WINO_ND_GENERIC=1: every plan takes the generic multi-pass transforms (dev / test knob)
 static bool force_generic() {
@@ -431,7 +477,9 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   if (tc) {
     e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
                         p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
-    if (e == cudaSuccess) e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K, p->V);
+    if (e == cudaSuccess && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32) plan_fold(p);
+    if (e == cudaSuccess && !p->fold_F)
+      e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K, p->V);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
@@ -727,7 +775,10 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(ps.end());
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
-    if (p->gemm_mode == WINO_GEMM_FFMA) {
+    if (p->fold_F) {
+      CUDA_TRY(launch_gemm_fold(p->tg, p->fold_bn, p->fold_g, p->fold_MO, p->M, (int)p->P, p->fold_Q, t_lo - g.t0,
+                                t_hi - g.t0, p->T_s, p->C, p->K, p->fold_tab, s));
+    } else if (p->gemm_mode == WINO_GEMM_FFMA) {
       CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, t_hi - g.t0, p->T_s, p->C, p->K, (int)p->K_s, s));
     } else {
       CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, t_lo - g.t0, t_hi - g.t0, p->T_s, p->C, p->K, s));
@@ -735,7 +786,9 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(pg.end());
     ProfScope po{p, s, 2};
     if (rec) CUDA_TRY(po.begin());
-    if (p->mixed) {
+    if (p->fold_F) {
+      CUDA_TRY(launch_output_fold(p->N, p->a, p->m, p->fold_F, p->spec, p->M, y, g, p->xp, s));
+    } else if (p->mixed) {
       CUDA_TRY(launch_output_mixed(p->N, p->a0, p->m0, p->a, p->m, p->M, y, g, p->xp,
                                    p->tm_M_ok ? &p->tm_M : nullptr, s));
     } else {
@@ -834,11 +887,11 @@ wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   int64_t launches = 3;
   if (p->tiny) launches = 1;
   else if (p->chunked) launches = 3 * (((int64_t)p->batch * p->geom.nbox0 + p->chunk_slabs - 1) / p->chunk_slabs);
-  const int64_t v[23] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[24] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
                          p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches,
-                         p->nd ? 0 : p->geom.nbox1};
+                         p->nd ? 0 : p->geom.nbox1, p->fold_F};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

@@ -147,6 +147,35 @@ __device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Lean issue of one chunk's 3xTF32 MMAs in TS mode (measured, tools/mma_bench.cu:
+// a kind::tf32 M=128 K=8 MMA occupies the tensor pipe N/2 cycles -- 16 at N = 32
+// -- but a loop that recomputes its operands each iteration issues one only
+// every ~54 cycles, so small-N GEMMs were issue-bound).  Fully unrolled over
+// the NK K=8 steps; the B descriptor is passed as its two 32-bit halves (the
+// start-address field sits in the low half and never carries out of it), so
+// each MMA needs one 32-bit add per operand.
+__device__ __forceinline__ void mma_ts_split(uint32_t d, uint32_t a_tmem, uint32_t b_lo32, uint32_t b_hi32,
+                                             uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\tmov.b64 bd, {%2, %3};\n\tsetp.ne.b32 p, %5, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], bd, %4, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "r"(b_lo32), "r"(b_hi32), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// d += V_lo U_hi + V_hi U_lo + V_hi U_hi over NK K=8 steps; A (V_hi at a_hi,
+// V_lo at a_lo) in TMEM, U_hi / U_lo descriptors (low halves bh / bl, shared
+// high half bhi32); `first`: the chunk opens the accumulation (D overwritten).
+template <int NK>
+__device__ __forceinline__ void mma3_chunk_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t bh, uint32_t bl,
+                                              uint32_t bhi32, uint32_t idesc, bool first) {
+#pragma unroll
+  for (int j = 0; j < NK; ++j) {
+    mma_ts_split(d, a_lo + 8 * j, bh + 64 * j, bhi32, idesc, (j == 0 && first) ? 0u : 1u);
+    mma_ts_split(d, a_hi + 8 * j, bl + 64 * j, bhi32, idesc, 1u);
+    mma_ts_split(d, a_hi + 8 * j, bh + 64 * j, bhi32, idesc, 1u);
+  }
+}
+
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])

@@ -137,7 +137,10 @@ def _oracle_stages(cfg, x, g, T):
 
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_stage_parity(name):
+def test_stage_parity(name, monkeypatch):
+    # the unfused pipeline's workspace (V, M); the folded GEMM's W is checked
+    # in tests/test_gpu_fold.py
+    monkeypatch.setenv("WINO_FOLD", "0")
     cfg = SMALL[name]
     x, g, y, plan = run(cfg)
     info = plan.info
@@ -269,6 +272,7 @@ def test_output_tma_ring_matches_plain(name, monkeypatch):
     y_tma, _ = _run_env(cfg, monkeypatch)
     y_ld, _ = _run_env(cfg, monkeypatch, WINO_OUT_TMA="0")
     assert torch.equal(y_tma, y_ld)
+    monkeypatch.setenv("WINO_FOLD", "0")
     x, g = make_inputs(cfg)
     monkeypatch.setenv("WINO_CHUNK_MB", "0.05")
     plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, cfg.batch, cfg.padding, fuse=4)
@@ -283,6 +287,8 @@ def test_output_tma_ring_matches_plain(name, monkeypatch):
 def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
     # the L2-chunked pipeline (fuse=4) runs the same per-tile arithmetic over
     # slab ranges with chunk-local V/M rows: identical bits for any chunking
+    # (compared with the unfused pipeline: chunked plans do not fold, a5)
+    monkeypatch.setenv("WINO_FOLD", "0")
     cfg = SMALL[name]
     x, g, y0, plan = run(cfg)
     plan.close()
@@ -294,6 +300,8 @@ def test_l2_chunked_matches_unchunked(name, chunk_mb, monkeypatch):
 
 
 def _run_env(cfg, monkeypatch, **env):
+    # bit-identity tests of the unfused kernels' variants: no a5 fold unless asked
+    env.setdefault("WINO_FOLD", "0")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _, _, y, plan = run(cfg)
