@@ -71,6 +71,7 @@ struct KGeom {
   int npl;                   // slabs per CTA (consecutive work items, one TMA box each)
   int in_threads;            // block size of the input kernel (<= 256; <= 512 in H mode)
   int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
+  int in_flags;              // dev A/B knob of the input kernel (WINO_IN_FLAGS; 0 in production)
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

@@ -98,6 +98,8 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
     g.in_threads = (atoi(ev) + 31) / 32 * 32;
     g.in_threads = g.in_threads < 64 ? 64 : g.in_threads > tmax ? tmax : g.in_threads;
   }
+  g.in_flags = 0;
+  if (const char* ev = getenv("WINO_IN_FLAGS")) g.in_flags = atoi(ev);  // dev A/B knob
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(g.slot_bytes + hb);

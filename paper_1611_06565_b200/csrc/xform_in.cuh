@@ -285,8 +285,12 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // (alpha_0 = 1, F(1,1): the axis-0 pass is the identity and is skipped;
       // phase 2 then reads the slab rows at their D offset)
       if constexpr (A0 > 1) {
+      // rows r = p * e1 + y walked with (p, y) stepped incrementally (a
+      // run-time division per row was a fifth of this pass's instructions)
+      int p = 0, y = warp;
+      while (y >= e1) { y -= e1; ++p; }
       for (int r = warp; r < npl * e1; r += nwarps) {
-        const int p = r / e1, y = r - p * e1;
+        if (g.in_flags & 2) { p = r / e1; y = r - p * e1; }   // dev A/B: the plain division
         ensure(p);
         float* row = S0 + p * slab_f + y * g.sst[1];
         for (int xb = 0; xb < e2; xb += 32) {  // every lane runs every pass (warp-wide sync below)
@@ -313,6 +317,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           }
           __syncwarp();  // writes of this pass before the next pass's reads
         }
+        y += nwarps;
+        while (y >= e1) { y -= e1; ++p; }
       }
       }
       __syncthreads();
@@ -321,12 +327,27 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // (npl planes are adjacent in t) into each of the alpha^2 planes of V
       // it touches (measured: the V store pattern bounds this kernel)
       const int R = tl1 * tl2, nrun = npl * R;
-      for (int u = threadIdx.x; u < A0 * nrun; u += blockDim.x) {
-        const int xi0 = u / nrun;
-        const int w = u - xi0 * nrun;
-        const int p = w / R;
-        const int tl = w - p * R;
-        const int t1 = tl / tl2, t2 = tl - t1 * tl2;
+      // item u = ((xi0 * npl + p) * tl1 + t1) * tl2 + t2, stepped by the block
+      // size with mixed-radix carries (three run-time divisions per item
+      // otherwise); the step's digits are computed once
+      const int ustep = blockDim.x;
+      const int st2 = ustep % tl2, st1 = (ustep / tl2) % tl1, stp = (ustep / R) % npl, sxi = ustep / nrun;
+      int xi0, p, t1, t2;
+      {
+        const int u0 = threadIdx.x;
+        xi0 = u0 / nrun;
+        p = (u0 / R) % npl;
+        t1 = (u0 / tl2) % tl1;
+        t2 = u0 % tl2;
+      }
+      for (int u = threadIdx.x; u < A0 * nrun; u += ustep) {
+        if (g.in_flags & 1) {   // dev A/B: the plain divisions
+          xi0 = u / nrun;
+          p = (u / R) % npl;
+          t1 = (u / tl2) % tl1;
+          t2 = u % tl2;
+        }
+        const int tl = t1 * tl2 + t2;
         const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
         float h[A * A];
         if constexpr (A0 == 1) ensure(p);
@@ -337,6 +358,17 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
         for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
+        // next item: add the step digit by digit (t2 fastest)
+        t2 += st2;
+        int cy = t2 >= tl2;
+        t2 -= cy ? tl2 : 0;
+        t1 += st1 + cy;
+        cy = t1 >= tl1;
+        t1 -= cy ? tl1 : 0;
+        p += stp + cy;
+        cy = p >= npl;
+        p -= cy ? npl : 0;
+        xi0 += sxi + cy;
       }
       return;
     }
