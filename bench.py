@@ -151,27 +151,39 @@ def tf32_peak(peaks):
     return max(nominal, peaks.get("tf32_measured") or 0.0)
 
 
-def gemm_tensor_util(cfg, B, ms, peaks):
-    """Tensor-pipe utilisation of the per-point GEMM: 3 TF32 products per fp32
-    multiply-add (3xTF32), 3 * 2 alpha^N T C K / (t * TF32 peak)."""
-    return 3 * cfg.winograd_gemm_flops(B) / (ms * 1e-3) / 1e12 / tf32_peak(peaks)
+WINO_GEMM_3XF16 = 4
 
 
-def roofline_for(cfg, B, stage, ms, peaks):
+def gemm_pipe_peak(peaks, gemm_mode=3):
+    """Dense peak (TFLOP/s) of the tensor kind the GEMM scheme runs on: TF32
+    for 3xTF32, the measured bf16 peak (= f16 dense rate) for 3xFP16."""
+    return peaks["bf16"] if gemm_mode == WINO_GEMM_3XF16 else tf32_peak(peaks)
+
+
+def gemm_tensor_util(cfg, B, ms, peaks, gemm_mode=3):
+    """Tensor-pipe utilisation of the per-point GEMM: 3 tensor products per
+    fp32 multiply-add (3xTF32 or 3xFP16), 3 * 2 alpha^N T C K / (t * peak of
+    that tensor kind)."""
+    return 3 * cfg.winograd_gemm_flops(B) / (ms * 1e-3) / 1e12 / gemm_pipe_peak(peaks, gemm_mode)
+
+
+def roofline_for(cfg, B, stage, ms, peaks, gemm_mode=3):
     t = ms * 1e-3
     nbytes = stage_bytes(cfg, B)[stage]
-    tf32 = tf32_peak(peaks)
+    tf32 = gemm_pipe_peak(peaks, gemm_mode)
     if stage == "gemm":
         flops = cfg.winograd_gemm_flops(B)
         t_mem = nbytes / (peaks["hbm_gbs"] * 1e9)
         t_tc = flops / (tf32 / 3 * 1e12)
-        util = round(gemm_tensor_util(cfg, B, ms, peaks), 4)
+        util = round(gemm_tensor_util(cfg, B, ms, peaks, gemm_mode), 4)
         if t_tc > t_mem:
             ach = flops / t / 1e12
             return {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32 / 3, 1), "unit": "TFLOP/s",
                     "frac": round(ach / (tf32 / 3), 4), "traffic": None, "tensor_util": util,
-                    "note": "fp32 flops of the per-point GEMM vs the 3xTF32 fp32-equivalent peak = TF32 peak / 3; "
-                            "TF32 peak = max(on-box cuBLAS TF32, bf16 %s x 1.1/2.25)" % peaks["source"]}
+                    "note": ("fp32 flops of the per-point GEMM vs the 3xFP16 fp32-equivalent peak = f16 (= bf16 %s) "
+                             "dense peak / 3" % peaks["source"]) if gemm_mode == WINO_GEMM_3XF16 else
+                            ("fp32 flops of the per-point GEMM vs the 3xTF32 fp32-equivalent peak = TF32 peak / 3; "
+                             "TF32 peak = max(on-box cuBLAS TF32, bf16 %s x 1.1/2.25)" % peaks["source"])}
         ach = nbytes / t / 1e9
         return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None, "tensor_util": util}
@@ -571,8 +583,10 @@ def cfg_dict(cfg, B, world, scaling, fuse=0):
             "F": "F(%d^%d,%d^%d)" % (cfg.m, cfg.N, cfg.r, cfg.N), "per_gpu_batch": B,
             "global_batch": B * world if scaling == "weak" else cfg.batch, "seq_len": None,
             "parallelism": par,
-            "gemm": "3xTF32 tcgen05 (TMEM fp32 accumulate); variant timed at plan creation "
-                    "(0 SMEM-A, 1 TMEM-A, 2 CTA-pair cta_group::2)",
+            "gemm": "tcgen05, TMEM fp32 accumulation; scheme per config (configs.*.gemm_scheme): 3xTF32 (variant "
+                    "timed at plan creation: 0 SMEM-A, 1 TMEM-A, 2 CTA-pair) or 3xFP16 (power-of-two scaled fp16 "
+                    "hi/lo split on kind::f16, CTA pairs) where measured faster; F(2^N,3^N), N >= 3: output "
+                    "transform of the 2 innermost axes in the GEMM epilogue (a5)",
             "pipeline": "L2-chunked a2->a3->a4" if fuse & 4 else "three kernels, V/M via HBM",
             "l2": ("flushed: 256 MiB memset + 256 MiB read (cold, clean L2) between timed steps, "
                    "outside the per-step events") if os.environ.get("WINO_BENCH_DIRTY_FLUSH", "0") != "1"
@@ -676,7 +690,8 @@ def main():
         for name, r in res.items():
             st = r["stages_ms"]
             dom = max(st, key=st.get)
-            rl = roofline_for(r["cfg_local"], r["B"], dom, st[dom], peaks)
+            gm = r["info"]["gemm_mode"]
+            rl = roofline_for(r["cfg_local"], r["B"], dom, st[dom], peaks, gm)
             rl["kernel"] = dom
             tk = traffic.get(name, {}).get(dom)
             if tk is not None:
@@ -687,7 +702,7 @@ def main():
                 if v <= 0:
                     per_stage[sname] = {"ms": 0.0, "note": "fused into the single-kernel tiny path"}
                     continue
-                rf = roofline_for(r["cfg_local"], r["B"], sname, v, peaks)
+                rf = roofline_for(r["cfg_local"], r["B"], sname, v, peaks, gm)
                 per_stage[sname] = {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
                 if sname == "gemm":
                     per_stage[sname]["tensor_util"] = rf["tensor_util"]
@@ -695,6 +710,7 @@ def main():
                              "stages": per_stage, "dominant": rl,
                              "filter_transform_ms": None if r["filter_ms"] is None else round(r["filter_ms"], 4),
                              "e2e_tflops": round(r["e2e_tflops"], 3), "e2e_ms": round(r["e2e_ms"], 4),
+                             "gemm_scheme": {3: "3xTF32", 4: "3xFP16 (scaled split)", 1: "FFMA"}.get(gm, str(gm)),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
                                                                  "chunk_slabs", "gemm_variant", "in_slab_tiles",
                                                                  "in_planes_per_cta", "axis_mode", "tiny", "fold", "in_bands")}}

@@ -70,7 +70,11 @@ enum {
   WINO_GEMM_AUTO = 0,   /* = WINO_GEMM_3XTF32 */
   WINO_GEMM_FFMA = 1,   /* CUDA-core fp32 FMA, smem-tiled */
   WINO_GEMM_1XTF32 = 2, /* single tf32 product: debug/accuracy experiments only */
-  WINO_GEMM_3XTF32 = 3  /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, TMEM fp32 accumulators */
+  WINO_GEMM_3XTF32 = 3, /* tcgen05 kind::tf32, hi*hi + hi*lo + lo*hi, TMEM fp32 accumulators */
+  WINO_GEMM_3XF16 = 4   /* tcgen05 kind::f16 (2x the tf32 rate): V, U scaled by powers of two
+                           (max|V| from the input transform, max|U| from the filter transform)
+                           and split into fp16 hi + lo; hi*hi + hi*lo + lo*hi, fp32 accumulators;
+                           single-(m, r) fused plans with K > 64, k-chunk 32 or 64 */
 };
 
 /* Activation f of Eq. (2) for wino_forward_ex. */

@@ -32,6 +32,10 @@ made explicit (reading #7):
                         and added to a float32 accumulator with one
                         round-to-nearest-even,
    * ``"1xtf32_k8"``:   V_hi U_hi only (what a single TF32 product gives);
+   * ``"3xf16_k16"``:   the kind::f16 scheme (gemm_f16.cu): V and U scaled by
+                        powers of two to a largest magnitude <= 2^15 and split
+                        into fp16 hi + lo (round to nearest even), three
+                        products per block of 16 channels, fp32 accumulation;
 5. inverse transform y = S_hat x_n A_n in float32.
 
 The tensor core's internal K=8 summation precision and its TMEM accumulation
@@ -126,6 +130,28 @@ def gemm_model(Vp: np.ndarray, Up: np.ndarray, mode: str) -> np.ndarray:
         for c in range(M):
             acc = (acc + np.outer(Vp[:, c], Up[c]).astype(np.float32)).astype(np.float32)
         return acc
+    if mode == "3xf16_k16":
+        # the kind::f16 scheme: V and U scaled by powers of two so that their
+        # largest magnitude is <= 2^15, each split into fp16 hi + lo (round to
+        # nearest even); per block of 16 channels lo*hi + hi*lo + hi*hi summed
+        # exactly, one fp32 rounding into the accumulator; result scaled back
+        def split16(a):
+            a = np.asarray(a, dtype=np.float32)
+            m = float(np.abs(a).max()) if a.size else 0.0
+            s = 0 if m == 0.0 else int(np.floor(np.log2(m))) + 1 - 15
+            sc = np.float32(2.0 ** -s)
+            a2 = (a * sc).astype(np.float32)
+            hi = a2.astype(np.float16)
+            lo = (a2 - hi.astype(np.float32)).astype(np.float16)
+            return hi.astype(np.float64), lo.astype(np.float64), s
+        vh, vl, sv = split16(Vp)
+        uh, ul, su = split16(Up)
+        acc = np.zeros((T, K), dtype=np.float32)
+        for c0 in range(0, M, 16):
+            b = slice(c0, min(M, c0 + 16))
+            blk = vl[:, b] @ uh[b] + vh[:, b] @ ul[b] + vh[:, b] @ uh[b]
+            acc = (acc.astype(np.float64) + blk).astype(np.float32)
+        return (acc.astype(np.float64) * 2.0 ** (sv + su)).astype(np.float32)
     if mode in ("3xtf32_k8", "1xtf32_k8"):
         vh, vl = split_tf32(Vp)
         uh, ul = split_tf32(Up)

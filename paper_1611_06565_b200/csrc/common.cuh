@@ -72,6 +72,10 @@ struct KGeom {
   int in_threads;            // block size of the input kernel (<= 256; <= 512 in H mode)
   int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
   int in_flags;              // dev A/B knob of the input kernel (WINO_IN_FLAGS; 0 in production)
+  // 3xFP16 GEMM scaling (gemm_f16.cu): a2 atomically maxes |V| into *vmax,
+  // a4 resets *vmax_reset = 0 for the next forward (NULL = not used)
+  unsigned int* vmax;
+  unsigned int* vmax_reset;
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

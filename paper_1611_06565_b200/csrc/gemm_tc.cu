@@ -300,6 +300,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   } else if (warp < 8) {  // warps 4-7 ------------------ epilogue
     const int q = warp - 4;
+    const uint64_t pol = l2_policy(true);
     uint32_t acc = 0, aph = 0;
     for (long long u = u_beg; u < u_end; u += u_step) {
       const int xi = (int)(u / per_xi);
@@ -317,28 +318,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (l2hint) {  // M stays in L2 for a4 (evict-last)
-            const uint64_t pol = l2_policy(true);
-            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
-              p += T_s;
-            }
-          } else if (full_n) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          } else {
-            const int kr = K - nb * BN - cb * 32;  // valid rows in this 32-block
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          }
+          // M stays in L2 for a4 (evict-last policy)
+          store_m32<false>(p, r, T_s, full_n ? 32 : K - nb * BN - cb * 32, l2hint, pol, 1.f);
         }
       }
       tc_fence_before();
@@ -624,6 +605,7 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   } else if (warp < 8) {  // warps 4-7 ------------------ epilogue
     const int q = warp - 4;
+    const uint64_t pol = l2_policy(true);
     uint32_t acc = 0, aph = 0;
     for (long long u = u_beg; u < u_end; u += u_step) {
       const int xi = (int)(u / per_xi);
@@ -640,28 +622,8 @@ k_gemm_ts(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T && !(dbg & 1)) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (l2hint) {  // M stays in L2 for a4 (evict-last)
-            const uint64_t pol = l2_policy(true);
-            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
-              p += T_s;
-            }
-          } else if (full_n) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          } else {
-            const int kr = K - nb * BN - cb * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          }
+          // M stays in L2 for a4 (evict-last policy)
+          store_m32<false>(p, r, T_s, full_n ? 32 : K - nb * BN - cb * 32, l2hint, pol, 1.f);
         }
       }
       tc_fence_before();

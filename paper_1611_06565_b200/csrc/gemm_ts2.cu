@@ -30,63 +30,6 @@ namespace wino {
 namespace tc {
 namespace {
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// shared::cluster address of `addr` (own shared::cta address) in CTA `rank`
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// wait with cluster-scope acquire: for barriers the peer CTA arrives on
-__device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-// Arrive on a barrier of a CTA of the cluster (cl_addr from mapa).  Default
-// (.release, .cta) semantics: the data it publishes is TMEM content ordered by
-// tcgen05.wait::st + tcgen05.fence::before_thread_sync, not generic memory,
-// and an explicit .release.cluster costs a CTA-wide MEMBAR per arrive.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cl_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
-}
-// TMA whose complete_tx lands on a barrier of the pair's leader (cl_bar).
-__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                                 uint32_t cl_bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(cl_bar)
-      : "memory");
-}
-__device__ __forceinline__ void tc2_commit_mc(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
-__device__ __forceinline__ void tc2_mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                                uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
 // kind::tf32, D f32, A K-major (TMEM), B MN-major, M = 256 (pair), N = BN.
 template <int BN>
 __host__ __device__ constexpr uint32_t idesc_tf32_pair() {
@@ -97,7 +40,7 @@ template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
 k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
            const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
-           int C, int K, int kc, int three, int nraw, int nbr, int dbg, int l2hint) {
+           int C, int K, int kc, int three, int nraw, int nbr, int dbg, int l2hint, int nbfast) {
   constexpr int HN = BN / 2;  // U columns loaded by each CTA
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sraw = smem_u32(smem_raw);
@@ -175,7 +118,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       uint32_t ph = 0;
       for (long long u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / per_xi);
-        const int mp = (int)(u % per_xi) % n_mp;
+        const int mp = nbfast ? (int)(u % per_xi) / n_nblk : (int)(u % per_xi) % n_mp;
         const int row0 = t_lo + mp * 2 * BM + (int)rank * BM;
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(rempty(s), ph ^ 1u);
@@ -197,7 +140,7 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
       const uint32_t half_tx = (three ? 2u : 1u) * hb_bytes;
       for (long long u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / per_xi);
-        const int nb = (int)(u % per_xi) / n_mp;
+        const int nb = nbfast ? (int)(u % per_xi) % n_nblk : (int)(u % per_xi) / n_mp;
         const int col0 = nb * BN + (int)rank * HN;
         for (int ch = 0; ch < n_chunks; ++ch) {
           mbar_wait(uempty(s), ph ^ 1u);
@@ -304,11 +247,12 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
   } else if (warp < 8) {  // warps 4-7 ------------------ epilogue: own 128 rows
     const int q = warp - 4;
     const uint32_t tempty_l[2] = {mapa(tempty(0), 0), mapa(tempty(1), 0)};
+    const uint64_t pol = l2_policy(true);
     uint32_t acc = 0, aph = 0;
     for (long long u = u_beg; u < total; u += u_step) {
       const int xi = (int)(u / per_xi);
       const int rr = (int)(u % per_xi);
-      const int nb = rr / n_mp, mp = rr % n_mp;
+      const int nb = nbfast ? rr % n_nblk : rr / n_mp, mp = nbfast ? rr / n_nblk : rr % n_mp;
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
       const int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
@@ -320,28 +264,8 @@ k_gemm_ts2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + cb * 32, r);
         if (t < T && !(dbg & 1)) {
           float* p = out + (long long)cb * 32 * T_s;
-          if (l2hint) {  // M stays in L2 for a4
-            const uint64_t pol = l2_policy(true);
-            const int kr = full_n ? 32 : K - nb * BN - cb * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) st_hint(p, __uint_as_float(r[j]), pol);
-              p += T_s;
-            }
-          } else if (full_n) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          } else {
-            const int kr = K - nb * BN - cb * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < kr) __stcs(p, __uint_as_float(r[j]));
-              p += T_s;
-            }
-          }
+          // M stays in L2 for a4 (evict-last policy)
+          store_m32<false>(p, r, T_s, full_n ? 32 : K - nb * BN - cb * 32, l2hint, pol, 1.f);
         }
       }
       tc_fence_before();
@@ -387,6 +311,18 @@ bool ts2_supported(int bn, int kc) {
   int nr, nb;
   size_t by;
   return bn >= 64 && bn <= 256 && 2 * bn + 4 * kc <= 512 && ts2_smem(bn, kc, &nr, &nb, &by);
+}
+
+// Unit order within a point: n-block fastest (1, default: the pairs that
+// share an m-pair's V run side by side, so its second n-block reads V from
+// L2) or m-pair fastest (0); WINO_GEMM_NBFAST overrides (dev knob)
+int gemm_nbfast() {
+  static int v = -1;
+  if (v < 0) {
+    const char* ev = getenv("WINO_GEMM_NBFAST");
+    v = ev ? (atoi(ev) != 0) : 1;
+  }
+  return v;
 }
 
 template <int BN>
@@ -447,7 +383,7 @@ static cudaError_t launch_ts2_bn(const TcGemm& tg, float* Mo, int P, int t_lo, i
   if (pairs < 1) return cudaSuccess;
   const long long Ts = T_s;
   return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, tg.tmA_ts, tg.tmBhi, tg.tmBlo, Mo, P,
-                    t_lo, T, Ts, C, K, tg.kc, tg.three, nraw, nbr, tg.dbg, l2hint);
+                    t_lo, T, Ts, C, K, tg.kc, tg.three, nraw, nbr, tg.dbg, l2hint, gemm_nbfast());
 }
 
 cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,

@@ -77,8 +77,19 @@ cudaError_t tc_gemm_prepare(TcGemm& tg, const float* V, const float* Uhi, const 
 // Vw: the plan's V buffer, rewritten (zeros) before each timed launch (NULL = no)
 cudaError_t tc_gemm_tune(TcGemm& tg, float* Mo, int P, int64_t T, int64_t T_s, int C, int K, float* Vw);
 bool ts2_supported(int bn, int kc);
+int gemm_nbfast();   // unit order of the CTA-pair GEMMs (n-block fastest: 1)
 cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                             cudaStream_t s);
+// a3 with the 3xFP16 scaled split on kind::f16 (gemm_f16.cu), CTA pairs, BN 128
+bool f16_supported(int K, int kc);
+cudaError_t f16_encode_u(CUtensorMap* tm, const void* base, int64_t K_s, int C, int P, int kc);
+cudaError_t launch_gemm_f16(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16, float* Mo,
+                            int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K, const unsigned int* vmax,
+                            const float* uscal, cudaStream_t s);
+// U (fp32) -> scaled fp16 hi / lo halves; *uscal = 2^su (mx: scratch word)
+cudaError_t launch_split16(const float* u32, int64_t n, unsigned int* mx, void* hi, void* lo, float* uscal,
+                           cudaStream_t s);
+
 // a3 with the output transform of the F innermost axes folded into the
 // epilogue (gemm_fold.cu): W[xo][o][k][t] = sum_q prod_f A^T[o_f][q_f] D_{xo*Q+q}
 // (Q = alpha^F points q, MO = m^F outputs o), W [P/Q * MO][K][T_s].

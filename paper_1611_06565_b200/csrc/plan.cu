@@ -225,6 +225,16 @@ struct wino_plan_s {
   // (gemm_fold.cu); the M buffer then holds W [P/Q * MO][K][T_s]
   int fold_F = 0, fold_Q = 1, fold_MO = 1, fold_bn = 0, fold_g = 0;
   FoldTab fold_tab{};
+  // 3xFP16 GEMM (gemm_f16.cu): U as scaled fp16 halves in ubuf (hi | lo |
+  // tail: uscal, umax | fp32 staging of the filter transform), vmax: max|V|
+  // word (a2 maxes it, the GEMM reads it, a4 clears it)
+  bool f16 = false;
+  void *U16hi = nullptr, *U16lo = nullptr;
+  float* uscal = nullptr;
+  unsigned int* umax = nullptr;
+  float* U32tmp = nullptr;
+  unsigned int* vmax = nullptr;
+  CUtensorMap tmBhi16{}, tmBlo16{};
   bool prof = false;
   int prof_calls = 0;
   std::vector<cudaEvent_t> ev;  // pool; prof_stage[i] tags pair (2i, 2i+1)
@@ -307,6 +317,24 @@ static void plan_fold(wino_plan_s* p) {
   p->fold_g = g;
 }
 
+// WINO_GEMM_AUTO's scheme for a fused-kernel plan: 3xTF32 unless the 3xFP16
+// split (twice the tensor rate) applies; WINO_GEMM_AUTO_MODE=3/4 overrides
+// (dev knob).  See fold_default / DESIGN.md for the measurements.
+static int auto_gemm_mode(int N, int a, int m, int C, int K, bool mixed, int fuse) {
+  (void)N; (void)a; (void)m; (void)mixed;
+  const bool f16_ok = K > 64 && C >= 32 && !(fuse & WINO_FUSE_L2_CHUNK);   // (f16_supported, checked again later)
+  if (const char* ev = getenv("WINO_GEMM_AUTO_MODE")) {
+    const int v = atoi(ev);
+    return v == WINO_GEMM_3XF16 && f16_ok ? v : WINO_GEMM_3XTF32;
+  }
+  // 3xFP16 where measured faster (tools/nbfast.sh, B200, ms per layer): c4
+  // (C = K = 256) 0.733 -> 0.685 (GEMM 0.369 -> 0.295: tensor-bound in
+  // 3xTF32), c2 (C = K = 128) 0.1034 -> 0.1011; not c3 (C = 64: 1.73 -> 1.80,
+  // the k-chunk of 32 leaves too little tensor work per handshake)
+  if (f16_ok && C >= 128 && K >= 128) return WINO_GEMM_3XF16;
+  return WINO_GEMM_3XTF32;
+}
+
 // WINO_ND_GENERIC=1: every plan takes the generic multi-pass transforms (dev / test knob)
 static bool force_generic() {
   const char* ev = getenv("WINO_ND_GENERIC");
@@ -324,7 +352,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   if (N < 1 || N > kMaxN) return fail(WINO_ERR_ARG, "N must be in 1..4 (got %d)", N);
   if (!dims) return fail(WINO_ERR_ARG, "dims is NULL");
   if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
-  if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
+  if (gemm_mode < 0 || gemm_mode > 4) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
   if (fuse & ~WINO_FUSE_L2_CHUNK) return fail(WINO_ERR_UNSUPPORTED, "fuse bitmask %d not implemented in this build", fuse);
   Transforms t, t0;
   int spec, spec0;
@@ -355,7 +383,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   p->N = N; p->m = m; p->r = r; p->a = a; p->C = C; p->K = K; p->batch = batch;
   p->mixed = mixed;
   p->m0 = m0; p->r0 = r0; p->a0 = a0;
-  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? WINO_GEMM_3XTF32 : gemm_mode;
+  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? auto_gemm_mode(N, a, m, C, K, mixed, fuse) : gemm_mode;
   p->fuse = fuse;
   p->spec = spec;
   if (const char* ev = getenv("WINO_IN_TMA")) p->use_tma_in = atoi(ev) != 0;
@@ -376,7 +404,8 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   if (T > (int64_t)INT32_MAX - 256) { delete p; return fail(WINO_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)T); }
   p->T_s = (T + 127) / 128 * 128;
   p->P = (int64_t)a0 * ipow(a, N - 1);
-  const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32;
+  p->f16 = p->gemm_mode == WINO_GEMM_3XF16;
+  const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32 || p->f16;
   const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
   p->K_s = tc ? (K + bn - 1) / bn * bn : (K + 31) / 32 * 32;
 
@@ -440,12 +469,15 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   }
   const size_t ucount = (size_t)p->P * C * p->K_s;
   const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
-  p->filter_bytes = ucount * 4 * nbuf;
+  p->filter_bytes = ucount * 4 * nbuf + (p->f16 ? 256 : 0);
   p->ws_bytes = ((size_t)p->P * C * p->T_s + (size_t)p->P * K * p->T_s) * 4;
   cudaError_t e = cudaMalloc(&p->ubuf, p->filter_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&p->V, p->ws_bytes);
+  if (e == cudaSuccess && p->f16) e = cudaMalloc(&p->vmax, 256);
+  if (e == cudaSuccess && p->f16) e = zero_private(p->vmax, 256);
   if (e != cudaSuccess) {
     cudaFree(p->ubuf);
+    cudaFree(p->vmax);
     delete p;
     cudaGetLastError();
     return fail(e == cudaErrorMemoryAllocation ? WINO_ERR_NOMEM : WINO_ERR_CUDA, "device allocation failed: %s",
@@ -474,11 +506,29 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     p->Ulo = p->ubuf + ucount;
   }
   p->filter_bcast_bytes = p->filter_bytes;
+  if (p->f16) {
+    // [hi16 | lo16 | tail 256 B | fp32 staging]; broadcast = hi, lo and the scale
+    uint8_t* b = reinterpret_cast<uint8_t*>(p->ubuf);
+    p->U16hi = b;
+    p->U16lo = b + ucount * 2;
+    p->uscal = reinterpret_cast<float*>(b + ucount * 4);
+    p->umax = reinterpret_cast<unsigned int*>(b + ucount * 4 + 4);
+    p->U32tmp = reinterpret_cast<float*>(b + ucount * 4 + 256);
+    p->filter_bcast_bytes = ucount * 4 + 256;
+  }
   if (tc) {
     e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
-                        p->gemm_mode == WINO_GEMM_3XTF32 ? 1 : 0, device);
+                        p->gemm_mode == WINO_GEMM_1XTF32 ? 0 : 1, device);
+    if (e == cudaSuccess && p->f16) {
+      if (p->chunked || !f16_supported(K, p->tg.kc)) {
+        wino_plan_destroy(p);
+        return fail(WINO_ERR_UNSUPPORTED, "3xFP16 GEMM needs K > 64, a k-chunk of 32 or 64 (C >= 32) and no L2 chunking");
+      }
+      e = f16_encode_u(&p->tmBhi16, p->U16hi, p->K_s, C, (int)p->P, p->tg.kc);
+      if (e == cudaSuccess) e = f16_encode_u(&p->tmBlo16, p->U16lo, p->K_s, C, (int)p->P, p->tg.kc);
+    }
     if (e == cudaSuccess && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32) plan_fold(p);
-    if (e == cudaSuccess && !p->fold_F)
+    if (e == cudaSuccess && !p->fold_F && !p->f16)
       e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K, p->V);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
@@ -515,7 +565,7 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
   if (N < 1 || N > kMaxN) return fail(WINO_ERR_ARG, "N must be in 1..4 (got %d)", N);
   if (!dims || !m || !r) return fail(WINO_ERR_ARG, "dims, m or r is NULL");
   if (C < 1 || K < 1 || batch < 1) return fail(WINO_ERR_ARG, "C, K, batch must be >= 1");
-  if (gemm_mode < 0 || gemm_mode > 3) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
+  if (gemm_mode < 0 || gemm_mode > 4) return fail(WINO_ERR_ARG, "bad gemm_mode %d", gemm_mode);
   bool uniform = true;
   for (int n = 1; n < N; ++n) uniform = uniform && m[n] == m[0] && r[n] == r[0];
   // equal axes: the single-(m, r) plan and its fused kernels
@@ -543,6 +593,8 @@ wino_status wino_plan_create_nd(wino_plan_t* plan_out, int N, const int64_t* dim
 static wino_status create_generic(wino_plan_t* plan_out, int N, const int64_t* dims, const int* m, const int* r,
                                   const char* points, int C, int K, int batch, const int* padding, int gemm_mode,
                                   int device) {
+  if (gemm_mode == WINO_GEMM_3XF16)
+    return fail(WINO_ERR_UNSUPPORTED, "3xFP16 GEMM only with the fused transform kernels (not the generic passes)");
   Transforms tn[kMaxN];
   int64_t P = 1;
   for (int n = 0; n < N; ++n) {
@@ -656,6 +708,7 @@ wino_status wino_plan_destroy(wino_plan_t p) {
   cudaFree(p->x_dev);
   cudaFree(p->y_dev);
   cudaFree(p->W);
+  cudaFree(p->vmax);
   for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
   if (p->s_in) {
     for (int i = 0; i < kHostChunks; ++i) {
@@ -674,7 +727,14 @@ wino_status wino_filter_transform(wino_plan_t p, const float* g, wino_stream_t s
   if (!p || !g) return fail(WINO_ERR_ARG, "NULL plan or filter pointer");
   DeviceGuard guard(p->device);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(launch_filter_xform(g, p->Uhi, p->Ulo, p->U32, p->fp, (cudaStream_t)stream));
+  if (p->f16) {
+    // fp32 U (one rounding from fp64) into the staging area, then the scaled fp16 split
+    CUDA_TRY(launch_filter_xform(g, nullptr, nullptr, p->U32tmp, p->fp, (cudaStream_t)stream));
+    CUDA_TRY(launch_split16(p->U32tmp, (int64_t)p->P * p->C * p->K_s, p->umax, p->U16hi, p->U16lo, p->uscal,
+                            (cudaStream_t)stream));
+  } else {
+    CUDA_TRY(launch_filter_xform(g, p->Uhi, p->Ulo, p->U32, p->fp, (cudaStream_t)stream));
+  }
   p->filter_ready = true;
   return WINO_OK;
 }
@@ -749,6 +809,10 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) ++p->prof_calls;
     return WINO_OK;
   }
+  if (p->f16) {
+    g.vmax = p->vmax;
+    g.vmax_reset = p->vmax;
+  }
   // TMA map of x, re-encoded when the input pointer or batch changes
   if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
     p->tm_x_ok = encode_input_map(&p->tm_x, x, g, p->N, B);
@@ -775,7 +839,10 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(ps.end());
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
-    if (p->fold_F) {
+    if (p->f16) {
+      CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->P, t_lo - g.t0, t_hi - g.t0, p->T_s, p->C,
+                               p->K, p->vmax, p->uscal, s));
+    } else if (p->fold_F) {
       CUDA_TRY(launch_gemm_fold(p->tg, p->fold_bn, p->fold_g, p->fold_MO, p->M, (int)p->P, p->fold_Q, t_lo - g.t0,
                                 t_hi - g.t0, p->T_s, p->C, p->K, p->fold_tab, s));
     } else if (p->gemm_mode == WINO_GEMM_FFMA) {

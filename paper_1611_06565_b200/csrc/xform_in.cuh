@@ -82,11 +82,18 @@ struct Ax0 {
   using Tab = Tab0_;
 };
 
+// Store one V value and track max|V| (the power-of-two scale of the 3xFP16
+// GEMM, gemm_f16.cu, is taken from it; one FMNMX per store).
+__device__ __forceinline__ void vput(float* p, float v, float& vm) {
+  *p = v;
+  vm = fmaxf(vm, fabsf(v));
+}
+
 // One work item: axis-0 output point X0 of one tile whose window starts at
 // slab offset `base` (+ D columns); writes alpha^(N-1) values of V.
 template <int N, int A, int M, class Tab, int D, int X0, class Ax>
 __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, const KGeom& g,
-                                        const XfParams& xp, float* __restrict__ vout, int64_t pstride) {
+                                        const XfParams& xp, float* __restrict__ vout, int64_t pstride, float& vm) {
   using Get = BTget<Tab>;
   using Get0 = BTget<typename Ax::Tab>;
   if constexpr (N == 1) {
@@ -94,7 +101,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     load_row<A, M, D>(S + base, h);
     all_axes<A, 1, A, A, Get>(h, xp);
 #pragma unroll
-    for (int j = 0; j < A; ++j) vout[j * pstride] = h[j];
+    for (int j = 0; j < A; ++j) vput(vout + j * pstride, h[j], vm);
   } else if constexpr (N == 2 && Ax::A == A && Ax::M == M) {
     // the whole alpha x alpha window in registers: every window row is read
     // once (no per-xi_0 re-reads), both axes transformed in place
@@ -103,7 +110,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     for (int i0 = 0; i0 < A; ++i0) load_row<A, M, D>(S + base + i0 * g.sst[0], h + i0 * A);
     all_axes<A, 2, A, A, Get>(h, xp);
 #pragma unroll
-    for (int j = 0; j < A * A; ++j) vout[j * pstride] = h[j];
+    for (int j = 0; j < A * A; ++j) vput(vout + j * pstride, h[j], vm);
   } else {
     constexpr int NL = N - 1;            // axes handled in registers
     constexpr int P1 = ipow(A, NL);      // values per work item
@@ -131,16 +138,16 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     }
     all_axes<A, NL, A, A, Get>(h, xp);
 #pragma unroll
-    for (int j = 0; j < P1; ++j) vout[(X0 * P1 + j) * pstride] = h[j];
+    for (int j = 0; j < P1; ++j) vput(vout + (X0 * P1 + j) * pstride, h[j], vm);
   }
 }
 
 template <int N, int A, int M, class Tab, int D, class Ax, int X0 = 0>
 __device__ __forceinline__ void in_dispatch(int xi0, const float* S, int base, const KGeom& g, const XfParams& xp,
-                                            float* vout, int64_t pstride) {
+                                            float* vout, int64_t pstride, float& vm) {
   if constexpr (X0 < Ax::A) {
-    if (xi0 == X0) in_work<N, A, M, Tab, D, X0, Ax>(S, base, g, xp, vout, pstride);
-    else in_dispatch<N, A, M, Tab, D, Ax, X0 + 1>(xi0, S, base, g, xp, vout, pstride);
+    if (xi0 == X0) in_work<N, A, M, Tab, D, X0, Ax>(S, base, g, xp, vout, pstride, vm);
+    else in_dispatch<N, A, M, Tab, D, Ax, X0 + 1>(xi0, S, base, g, xp, vout, pstride, vm);
   }
 }
 
@@ -242,7 +249,7 @@ struct PlaneInfo {
 template <int N, int A, int M, class Tab, int D, class Ax>
 __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int slab_f, float* __restrict__ H,
                                                  float* __restrict__ V, const KGeom& g, const XfParams& xp,
-                                                 const PlaneInfo* pl, int npl, uint32_t mb0) {
+                                                 const PlaneInfo* pl, int npl, uint32_t mb0, float& vm) {
   const int64_t pstride = (int64_t)g.C * g.T_s;
   // slab p's TMA box has landed once its mbarrier completes phase 0; every
   // thread waits only for the slabs of its own items, in order, so work on
@@ -357,7 +364,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         all_axes<A, 2, A, A, Get>(h, xp);
         float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
-        for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
+        for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
         // next item: add the step digit by digit (t2 fastest)
         t2 += st2;
         int cy = t2 >= tl2;
@@ -418,7 +425,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       all_axes<A, 2, A, A, Get>(h, xp);
       float* vo = vb + (t0l * tl1 + t1) * tl2 + t2 + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
-      for (int j = 0; j < A * A; ++j) vo[j * pstride] = h[j];
+      for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
     }
   } else if constexpr (A == 1 && M == 1 && N >= 2) {
     // ---- r = 1 on every axis but 0 (3x1x1-type kernels): a tile is one
@@ -458,7 +465,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
             first = false;
           }
         }
-        vo[x0 * pstride] = acc;
+        vput(vo + x0 * pstride, acc, vm);
       }
     }
   } else {
@@ -483,7 +490,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           base += ti * M * g.sst[ax];
         }
         base += rem * Ax::M * g.sst[0];
-        in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride);
+        in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride, vm);
       }
       return;
     }
@@ -506,7 +513,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         base += ti * M * g.sst[ax];
       }
       base += rem * Ax::M * g.sst[0];
-      in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride);
+      in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride, vm);
     }
   }
 }
@@ -570,8 +577,23 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
                                          pl[p].a1 * M);
     __syncthreads();
   }
+  float vm = 0.f;
   transform_planes<N, A, M, Tab, D, Ax>(smem_f, slab_f, H, V, g, xp, pl, npl,
-                                    kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u);
+                                    kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u, vm);
+  // max|V| of the whole launch (for the 3xFP16 GEMM's scale): block
+  // reduction, one atomicMax per CTA (non-negative floats order as uints)
+  if (g.vmax) {
+    __shared__ float wmax[32];
+    for (int o = 16; o; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = vm;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      vm = threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.f;
+      for (int o = 16; o; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+      if (threadIdx.x == 0) atomicMax(g.vmax, __float_as_uint(vm));
+    }
+  }
 }
 
 template <class K>

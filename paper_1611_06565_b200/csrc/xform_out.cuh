@@ -112,6 +112,8 @@ k_output_xform(const float* __restrict__ Mx, float* __restrict__ y, const __grid
   constexpr int MN = Ax::M * ipow(M, N - 1);
   pdl_wait();      // M comes from the GEMM
   pdl_trigger();
+  // the GEMM has consumed max|V| (3xFP16 scaling): clear it for the next forward
+  if (g.vmax_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *g.vmax_reset = 0u;
   const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
   const int k = blockIdx.y;
   if (t >= g.T) return;
@@ -176,6 +178,7 @@ k_output_xform_tma(float* __restrict__ y, const __grid_constant__ KGeom g, const
   __syncthreads();
   pdl_wait();      // M comes from the GEMM
   pdl_trigger();
+  if (g.vmax_reset && blockIdx.x == 0 && threadIdx.x == 0) *g.vmax_reset = 0u;   // (see k_output_xform)
   if (threadIdx.x == 0)
     for (int st = 0; st < ns; ++st) issue(st, st);
   int64_t q = 0;

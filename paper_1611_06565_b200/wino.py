@@ -26,7 +26,7 @@ WINO_ERR_STATE, WINO_ERR_UNSUPPORTED, WINO_ERR_CUDA, WINO_ERR_NOMEM = 5, 6, 7, 8
 STATUS_NAMES = {0: "WINO_OK", 1: "WINO_ERR_ARG", 2: "WINO_ERR_SHAPE", 3: "WINO_ERR_POINTS",
                 4: "WINO_ERR_SYNTH", 5: "WINO_ERR_STATE", 6: "WINO_ERR_UNSUPPORTED",
                 7: "WINO_ERR_CUDA", 8: "WINO_ERR_NOMEM"}
-WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32 = 0, 1, 2, 3
+WINO_GEMM_AUTO, WINO_GEMM_FFMA, WINO_GEMM_1XTF32, WINO_GEMM_3XTF32, WINO_GEMM_3XF16 = 0, 1, 2, 3, 4
 WINO_FUSE_NONE, WINO_FUSE_L2_CHUNK = 0, 4
 WINO_ACT_NONE, WINO_ACT_RELU = 0, 1
 

@@ -33,6 +33,8 @@ def test_roofline_bounds():
     t = bench.roofline_for(c4, c4.batch, "gemm", 0.4, PEAKS)
     assert t["bound"] == "tensor" and t["unit"] == "TFLOP/s"
     assert t["peak"] == pytest.approx(1600.0 * 1.1 / 2.25 / 3, rel=1e-3)      # 3xTF32 fp32-equivalent
+    f = bench.roofline_for(c4, c4.batch, "gemm", 0.3, PEAKS, 4)             # 3xFP16: f16 rate / 3
+    assert f["tensor_util"] == pytest.approx(3 * c4.winograd_gemm_flops() / 0.3e-3 / 1e12 / 1600.0, rel=1e-3)
     assert 0 < t["frac"] < 1.5
     o = bench.roofline_for(c4, c4.batch, "output_xform", 0.2, PEAKS)
     assert o["bound"] == "hbm"

@@ -82,7 +82,7 @@ def test_f64_mode_is_oracle_winograd(N, dims, m, r, pad):
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("mode", ["fp32", "fp32_seq", "3xtf32_k8", "1xtf32_k8"])
+@pytest.mark.parametrize("mode", ["fp32", "fp32_seq", "3xtf32_k8", "1xtf32_k8", "3xf16_k16"])
 def test_exact_when_nothing_rounds(mode):
     # small integers, F(2,3) with {0, 1, -1, inf}: every transform entry is
     # 0, +-1 or +-1/2 (in C; U is computed in float64) and every intermediate
@@ -156,3 +156,17 @@ def test_model_tolerance_shape():
     ref = direct.direct_conv_f64(x.numpy(), g.numpy(), 1)
     tl, tm, rel, mx = fm.model_tolerance(x.numpy(), g.numpy(), 1, 5, 4, ref)
     assert tl == fm.K_REL * rel and tm == fm.K_MAX * mx and 0 < rel < 1e-4
+
+
+def test_f16_split_model_matches_tf32_split_model():
+    # the 3xFP16 scheme keeps 22 significant bits per operand like the RNA
+    # 3xTF32 split: on a c4 slice both models land within a factor 2 of each
+    # other (and of SURVEY Appendix B's tensor-core model, pinned above)
+    cfg = _cfg1("c4")
+    x, g = make_inputs(cfg)
+    xn, gn = x.numpy(), g.numpy()[:32]
+    ref = direct.direct_conv_f64(xn, gn, cfg.pad)
+    r3, _ = fm.errors(fm.winograd_model(xn, gn, cfg.pad, 4, 3, None, "3xtf32_k8"), ref)
+    r16, _ = fm.errors(fm.winograd_model(xn, gn, cfg.pad, 4, 3, None, "3xf16_k16"), ref)
+    print("c4[K=32] 3xtf32_k8 %.3e 3xf16_k16 %.3e" % (r3, r16))
+    assert 0.5 * r3 <= r16 <= 2.0 * r3

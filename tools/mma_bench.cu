@@ -11,7 +11,22 @@
 
 using namespace wino::tc;
 
-template <int N, bool TS>
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+template <int N, bool TS, bool F16 = false>
 __global__ void __launch_bounds__(128, 1) k_mma_rate(unsigned long long* out, int L, int nacc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar;
@@ -36,7 +51,9 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(unsigned long long* out, in
   tc_fence_after();
   const uint32_t tm = holder;
   if (warp == 0) {
-    constexpr uint32_t idesc = TS ? idesc_tf32_ts<N>() : idesc_tf32<N>();
+    constexpr uint32_t idesc = F16 ? ((1u << 4) | (TS ? 0u : (1u << 15)) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+                                      ((uint32_t)(128 >> 4) << 24))
+                                   : TS ? idesc_tf32_ts<N>() : idesc_tf32<N>();
     const uint64_t db = sdesc(sb + 32768, 8u * 128u, 512u);   // B: 8 K-rows x N (MN-major)
     const uint64_t da = sdesc(sb, 8u * 128u, 512u);           // A (SS mode)
     const uint32_t a_t = tm + 256;                            // A columns in TMEM (TS mode)
@@ -49,8 +66,13 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(unsigned long long* out, in
           for (int i = 0; i < L; i += 16) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              if constexpr (TS) tc_mma_tf32_ts(tm, a_t, db, idesc, 1u);
-              else tc_mma_tf32(tm, da, db, idesc, 1u);
+              if constexpr (F16) {
+                if constexpr (TS) mma_f16_ts(tm, a_t, db, idesc, 1u);
+                else mma_f16_ss(tm, da, db, idesc, 1u);
+              } else {
+                if constexpr (TS) tc_mma_tf32_ts(tm, a_t, db, idesc, 1u);
+                else tc_mma_tf32(tm, da, db, idesc, 1u);
+              }
             }
           }
         } else {
@@ -76,11 +98,11 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(unsigned long long* out, in
   }
 }
 
-template <int N, bool TS>
+template <int N, bool TS, bool F16 = false>
 void run(int grid, int L, int nacc) {
   unsigned long long* d;
   cudaMalloc(&d, grid * 8);
-  auto k = k_mma_rate<N, TS>;
+  auto k = k_mma_rate<N, TS, F16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   k<<<grid, 128, 64 * 1024>>>(d, L, nacc);
   cudaError_t e = cudaDeviceSynchronize();
@@ -88,15 +110,20 @@ void run(int grid, int L, int nacc) {
   cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
   double mx = 0, sum = 0;
   for (int i = 0; i < grid; ++i) { sum += h[i]; if (h[i] > mx) mx = h[i]; }
-  printf("%s N=%3d grid=%3d nacc=%d L=%d: %6.1f cycles/MMA (mean), %6.1f (max)  %s\n", TS ? "TS" : "SS", N, grid, nacc,
+  printf("%s%s N=%3d grid=%3d nacc=%d L=%d: %6.1f cycles/MMA (mean), %6.1f (max)  %s\n", F16 ? "f16 " : "tf32 ",
+         TS ? "TS" : "SS", N, grid, nacc,
          L, sum / grid / L, mx / L, e == cudaSuccess ? "" : cudaGetErrorString(e));
   cudaFree(d);
 }
 
 int main() {
   const int L = 3008;
-  for (int grid : {1, 148}) {
-    for (int nacc : {0, 1}) {
+  run<128, true, true>(1, L, 0);
+  run<128, false, true>(1, L, 0);
+  run<256, true, true>(1, L, 0);
+  run<64, true, true>(1, L, 0);
+  for (int grid : {1}) {
+    for (int nacc : {0}) {
       run<32, true>(grid, L, nacc);
       run<64, true>(grid, L, nacc);
       run<128, true>(grid, L, nacc);
