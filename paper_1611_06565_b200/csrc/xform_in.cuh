@@ -82,11 +82,19 @@ struct Ax0 {
   using Tab = Tab0_;
 };
 
-// Store one V value and track max|V| (the power-of-two scale of the 3xFP16
-// GEMM, gemm_f16.cu, is taken from it; one FMNMX per store).
 __device__ __forceinline__ void vput(float* p, float v, float& vm) {
+  (void)vm;
   *p = v;
-  vm = fmaxf(vm, fabsf(v));
+}
+// max|V| of the stored values for the 3xFP16 GEMM's scale (g.vmax set): one
+// uniform test per work item, the FMNMX only in such plans (a per-store max
+// in every plan cost c2's input transform ~4%)
+template <int NV>
+__device__ __forceinline__ void vtrack(const KGeom& g, const float* h, float& vm) {
+  if (g.vmax) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) vm = fmaxf(vm, fabsf(h[j]));
+  }
 }
 
 // One work item: axis-0 output point X0 of one tile whose window starts at
@@ -102,6 +110,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     all_axes<A, 1, A, A, Get>(h, xp);
 #pragma unroll
     for (int j = 0; j < A; ++j) vput(vout + j * pstride, h[j], vm);
+    vtrack<A>(g, h, vm);
   } else if constexpr (N == 2 && Ax::A == A && Ax::M == M) {
     // the whole alpha x alpha window in registers: every window row is read
     // once (no per-xi_0 re-reads), both axes transformed in place
@@ -111,6 +120,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     all_axes<A, 2, A, A, Get>(h, xp);
 #pragma unroll
     for (int j = 0; j < A * A; ++j) vput(vout + j * pstride, h[j], vm);
+    vtrack<A * A>(g, h, vm);
   } else {
     constexpr int NL = N - 1;            // axes handled in registers
     constexpr int P1 = ipow(A, NL);      // values per work item
@@ -139,6 +149,7 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
     all_axes<A, NL, A, A, Get>(h, xp);
 #pragma unroll
     for (int j = 0; j < P1; ++j) vput(vout + (X0 * P1 + j) * pstride, h[j], vm);
+    vtrack<P1>(g, h, vm);
   }
 }
 
@@ -365,6 +376,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
         for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
+        vtrack<A * A>(g, h, vm);
         // next item: add the step digit by digit (t2 fastest)
         t2 += st2;
         int cy = t2 >= tl2;
@@ -426,6 +438,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       float* vo = vb + (t0l * tl1 + t1) * tl2 + t2 + (int64_t)xi0 * (A * A) * pstride;
 #pragma unroll
       for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
+      vtrack<A * A>(g, h, vm);
     }
   } else if constexpr (A == 1 && M == 1 && N >= 2) {
     // ---- r = 1 on every axis but 0 (3x1x1-type kernels): a tile is one
@@ -466,6 +479,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           }
         }
         vput(vo + x0 * pstride, acc, vm);
+        if (g.vmax) vm = fmaxf(vm, fabsf(acc));
       }
     }
   } else {
@@ -580,8 +594,8 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   float vm = 0.f;
   transform_planes<N, A, M, Tab, D, Ax>(smem_f, slab_f, H, V, g, xp, pl, npl,
                                     kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u, vm);
-  // max|V| of the whole launch (for the 3xFP16 GEMM's scale): block
-  // reduction, one atomicMax per CTA (non-negative floats order as uints)
+  // max|V| of the whole launch (the 3xFP16 GEMM's scale): block reduction,
+  // one atomicMax per CTA (non-negative floats order as their bit patterns)
   if (g.vmax) {
     __shared__ float wmax[32];
     for (int o = 16; o; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
