@@ -76,7 +76,6 @@ struct KGeom {
   // a4 resets *vmax_reset = 0 for the next forward (NULL = not used)
   unsigned int* vmax;
   unsigned int* vmax_reset;
-  float vbound;              // max|V| <= vbound * max|x| (product over axes of the largest B^T row 1-norm)
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

@@ -229,7 +229,6 @@ struct wino_plan_s {
   // tail: uscal, umax | fp32 staging of the filter transform), vmax: max|V|
   // word (a2 maxes it, the GEMM reads it, a4 clears it)
   bool f16 = false;
-  float vbound = 0.f;   // max|V| <= vbound * max|x| (largest B^T row 1-norm per axis, multiplied; rounded up)
   void *U16hi = nullptr, *U16lo = nullptr;
   float* uscal = nullptr;
   unsigned int* umax = nullptr;
@@ -508,21 +507,6 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   }
   p->filter_bcast_bytes = p->filter_bytes;
   if (p->f16) {
-    // the bound of max|V| by max|x|: the fp32 B^T the kernels use, row 1-norms
-    // in double, product over the axes (axis 0 may differ), 1 ulp of margin
-    double bnd = 1.0;
-    for (int n = 0; n < N; ++n) {
-      const FloatTables& ftn = n == 0 ? ft0 : ft;
-      const int an = n == 0 ? a0 : a;
-      double best = 0.0;
-      for (int i = 0; i < an; ++i) {
-        double s1 = 0.0;
-        for (int j = 0; j < an; ++j) s1 += fabs((double)ftn.BT[i][j]);
-        best = best > s1 ? best : s1;
-      }
-      bnd *= best;
-    }
-    p->vbound = (float)(bnd * (1.0 + 1e-6));
     // [hi16 | lo16 | tail 256 B | fp32 staging]; broadcast = hi, lo and the scale
     uint8_t* b = reinterpret_cast<uint8_t*>(p->ubuf);
     p->U16hi = b;
@@ -828,7 +812,6 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
   if (p->f16) {
     g.vmax = p->vmax;
     g.vmax_reset = p->vmax;
-    g.vbound = p->vbound;
   }
   // TMA map of x, re-encoded when the input pointer or batch changes
   if (p->use_tma_in && (x != p->tm_x_ptr || B != p->tm_x_B)) {
