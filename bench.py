@@ -135,11 +135,20 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
-def stage_bytes(cfg, B):
-    """Algorithmic (compulsory) bytes of each stage for B samples (DESIGN.md
-    Sec. 8), from the package's analytic cost model."""
+def stage_model_for(cfg, B, info=None):
+    """The package's analytic cost model of the plan as built (DESIGN.md
+    Sec. 8): with an a5 fold (info "fold" / "fold_mode") the GEMM writes and
+    a4 reads W instead of M, and the filter-side fold streams U' and executes
+    m^F x the multiply-adds."""
     from paper_1611_06565_b200.cost import stage_model
-    st = stage_model(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding)
+    info = info or {}
+    return stage_model(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, B, cfg.padding,
+                       fold=info.get("fold", 0), fold_mode=info.get("fold_mode", 0))
+
+
+def stage_bytes(cfg, B, info=None):
+    """Algorithmic (compulsory) bytes of each stage for B samples."""
+    st = stage_model_for(cfg, B, info)
     return {s: st[s]["bytes"] for s in ("input_xform", "gemm", "output_xform")}
 
 
@@ -160,22 +169,25 @@ def gemm_pipe_peak(peaks, gemm_mode=3):
     return peaks["bf16"] if gemm_mode == WINO_GEMM_3XF16 else tf32_peak(peaks)
 
 
-def gemm_tensor_util(cfg, B, ms, peaks, gemm_mode=3):
+def gemm_tensor_util(cfg, B, ms, peaks, gemm_mode=3, info=None):
     """Tensor-pipe utilisation of the per-point GEMM: 3 tensor products per
     fp32 multiply-add (3xTF32 or 3xFP16), 3 * 2 alpha^N T C K / (t * peak of
-    that tensor kind)."""
-    return 3 * cfg.winograd_gemm_flops(B) / (ms * 1e-3) / 1e12 / gemm_pipe_peak(peaks, gemm_mode)
+    that tensor kind); the multiply-adds the GEMM executes (m^F x under the
+    filter-side fold)."""
+    flops = stage_model_for(cfg, B, info)["gemm"]["flops"]
+    return 3 * flops / (ms * 1e-3) / 1e12 / gemm_pipe_peak(peaks, gemm_mode)
 
 
-def roofline_for(cfg, B, stage, ms, peaks, gemm_mode=3):
+def roofline_for(cfg, B, stage, ms, peaks, gemm_mode=3, info=None):
     t = ms * 1e-3
-    nbytes = stage_bytes(cfg, B)[stage]
+    sm = stage_model_for(cfg, B, info)
+    nbytes = sm[stage]["bytes"]
     tf32 = gemm_pipe_peak(peaks, gemm_mode)
     if stage == "gemm":
-        flops = cfg.winograd_gemm_flops(B)
+        flops = sm["gemm"]["flops"]
         t_mem = nbytes / (peaks["hbm_gbs"] * 1e9)
         t_tc = flops / (tf32 / 3 * 1e12)
-        util = round(gemm_tensor_util(cfg, B, ms, peaks, gemm_mode), 4)
+        util = round(gemm_tensor_util(cfg, B, ms, peaks, gemm_mode, info), 4)
         if t_tc > t_mem:
             ach = flops / t / 1e12
             return {"bound": "tensor", "achieved": round(ach, 2), "peak": round(tf32 / 3, 1), "unit": "TFLOP/s",
@@ -691,7 +703,7 @@ def main():
             st = r["stages_ms"]
             dom = max(st, key=st.get)
             gm = r["info"]["gemm_mode"]
-            rl = roofline_for(r["cfg_local"], r["B"], dom, st[dom], peaks, gm)
+            rl = roofline_for(r["cfg_local"], r["B"], dom, st[dom], peaks, gm, r["info"])
             rl["kernel"] = dom
             tk = traffic.get(name, {}).get(dom)
             if tk is not None:
@@ -702,7 +714,7 @@ def main():
                 if v <= 0:
                     per_stage[sname] = {"ms": 0.0, "note": "fused into the single-kernel tiny path"}
                     continue
-                rf = roofline_for(r["cfg_local"], r["B"], sname, v, peaks, gm)
+                rf = roofline_for(r["cfg_local"], r["B"], sname, v, peaks, gm, r["info"])
                 per_stage[sname] = {"ms": round(v, 5), **{k: rf[k] for k in ("bound", "achieved", "unit", "frac")}}
                 if sname == "gemm":
                     per_stage[sname]["tensor_util"] = rf["tensor_util"]
@@ -713,7 +725,7 @@ def main():
                              "gemm_scheme": {3: "3xTF32", 4: "3xFP16 (scaled split)", 1: "FFMA"}.get(gm, str(gm)),
                              "info": {k: r["info"][k] for k in ("T_per_sample", "n_points", "n_blk", "k_chunk",
                                                                  "chunk_slabs", "gemm_variant", "in_slab_tiles",
-                                                                 "in_planes_per_cta", "axis_mode", "tiny", "fold", "in_bands")}}
+                                                                 "in_planes_per_cta", "axis_mode", "tiny", "fold", "fold_mode", "in_bands")}}
         out["roofline"] = configs[args.config]["dominant"]
         out["roofline"]["peak_source"] = ("HBM: MEASURED_PEAKS.json (%s); tensor: TF32 = max(on-box cuBLAS "
                                           "TF32 %s, bf16 x 1.1/2.25)" % (

@@ -182,7 +182,7 @@ WINO_API wino_status wino_forward_host(wino_plan_t plan, const float* x_host, fl
 WINO_API wino_status wino_plan_out_dims(wino_plan_t plan, int64_t* out);
 /* Device bytes: workspace (V + M) and filter buffer (U_hi + U_lo). */
 WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, size_t* filter_bytes);
-/* info[0..24): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
+/* info[0..25): N, m, r, alpha, C, K, batch, T_per_sample, T_stride, n_points
  * (alpha^N), K_stride, gemm_mode, fuse, n_blk, k_chunk, chunk_slabs (0 =
  * unchunked), gemm_variant (0 SMEM-A, 1 TMEM-A, 2 CTA-pair; -1 FFMA; chosen by
  * timing the supported variants once in plan_create), input slab depth bt0,
@@ -192,7 +192,11 @@ WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, 
  * (kernel launches of one full-batch forward), in_bands (axis-1 bands of the
  * fused input transform's slab: 1 unbanded, > 1 for large N >= 3 planes, 0
  * on the generic path), fold (F > 0: the output transform of the F innermost
- * axes runs in the GEMM epilogue, a5; 0: unfused). */
+ * axes is folded into the GEMM, a5; 0: unfused), fold_mode (1: epilogue fold
+ * of the accumulators, gemm_fold.cu; 2: filter-side fold, A^T of those axes
+ * multiplied into the cached transformed filter U' at wino_filter_transform
+ * time and the GEMM run as (n_points / alpha^F) GEMMs of depth alpha^F * C
+ * and width m^F * K; 0: none). */
 WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
 
 /* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------

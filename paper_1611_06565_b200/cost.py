@@ -111,12 +111,18 @@ def arithmetic_intensity(T: int, M: int, K: int, fused: bool) -> Fraction:
 
 # ------------------------------------------------------------------ device
 def stage_model(N: int, dims: Sequence[int], m, r, C: int, K: int, B: int,
-                pad: Sequence[int] = None, hbm_gbs: float = None, tf32_tflops: float = None) -> Dict[str, dict]:
+                pad: Sequence[int] = None, hbm_gbs: float = None, tf32_tflops: float = None,
+                fold: int = 0, fold_mode: int = 0) -> Dict[str, dict]:
     """Algorithmic bytes / flops of the four stages of one forward (fp32,
     every tensor moved once) and, if peaks are given, the
     roofline time in ms of each stage (the GEMM at the 3xTF32 rate =
     tf32_tflops / 3 fp32-equivalent).  m and r may be per-axis sequences
-    (F(m_1 x .. x m_N, r_1 x .. x r_N), Eq. (4))."""
+    (F(m_1 x .. x m_N, r_1 x .. x r_N), Eq. (4)).
+
+    fold = F > 0 (a5, single (m, r)): the GEMM writes W, (m/alpha)^F of M's
+    size, and a4 reads W.  fold_mode 2 (the filter-side fold) reads U' = m^F
+    x U and executes m^F x the multiply-adds (zero coefficients included);
+    fold_mode 1 (epilogue fold) keeps U and the flops."""
     pad = tuple(pad) if pad is not None else (0,) * N
     mv = tuple(m) if isinstance(m, (list, tuple)) else (m,) * N
     rv = tuple(r) if isinstance(r, (list, tuple)) else (r,) * N
@@ -128,10 +134,17 @@ def stage_model(N: int, dims: Sequence[int], m, r, C: int, K: int, B: int,
     # U counted once in fp32 (the compulsory filter bytes; the 3xTF32 GEMM
     # streams its hi/lo halves, i.e. 2x this, from L2)
     Vb, Mb, Ub = 4 * P * C * T, 4 * P * K * T, 4 * P * C * K
+    gflops = 2 * P * T * C * K
+    if fold:
+        a, mm = mv[0] + rv[0] - 1, mv[0]
+        Mb = Mb * mm ** fold // a ** fold            # W
+        if fold_mode == 2:
+            Ub *= mm ** fold                          # U'
+            gflops *= mm ** fold
     st = {
         "filter_xform": {"bytes": 4 * K * C * math.prod(rv) + Ub, "flops": 0},
         "input_xform": {"bytes": xb + Vb, "flops": 0},
-        "gemm": {"bytes": Vb + Ub + Mb, "flops": 2 * P * T * C * K},
+        "gemm": {"bytes": Vb + Ub + Mb, "flops": gflops},
         "output_xform": {"bytes": Mb + yb, "flops": 0},
     }
     if hbm_gbs:

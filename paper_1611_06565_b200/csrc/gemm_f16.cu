@@ -319,6 +319,256 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
 }
 
+// V-resident variant for K = NB * BN with NB = 2 (k_gemm_f16n): a unit is
+// (xi, m-pair) and covers every n-block.  The unit's whole converted V block
+// (C / KC chunks, KC TMEM columns each) sits in TMEM next to NB accumulators
+// (NB * BN + C <= 512 columns), so V is loaded and converted once per unit
+// instead of once per n-block (k_gemm_f16p re-reads it through L2 and
+// converts it NB times).  Chunk slot c is released for the next unit's
+// conversion by the last n-block's MMA on it; accumulator nb is drained by
+// the epilogue while the MMAs of the next n-block run.  zmask bit nb*8 + c:
+// U chunk (nb, c) is zero by construction (filter-side fold, A^T_F[o][q] = 0
+// for every column of the n-block), its U load and MMAs are skipped.
+template <int BN, int KC, int NB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
+k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
+            const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
+            int C, int K, int nraw, int nbr, int l2hint, const unsigned int* __restrict__ vmax,
+            const float* __restrict__ uscal, int zmask) {
+  constexpr int HN = BN / 2;
+  static_assert(HN == 64, "one 64-wide fp16 swizzle group per CTA half");
+  constexpr int NKS = KC / 16;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (sraw & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  const uint32_t sbase = sraw + pad;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int n_chunks = (C + KC - 1) / KC;            // <= (512 - NB * BN) / KC (host-checked)
+  const uint32_t a_bytes = (uint32_t)BM * KC * 4;
+  const uint32_t hb_bytes = (uint32_t)HN * KC * 2;
+  const uint32_t raw0 = sbase;
+  const uint32_t ub0 = raw0 + nraw * a_bytes;
+  const uint32_t bar0 = ub0 + 2u * nbr * hb_bytes;
+  auto rfull = [&](int s) { return bar0 + 8u * s; };
+  auto rempty = [&](int s) { return bar0 + 8u * (nraw + s); };
+  auto ufull = [&](int s) { return bar0 + 8u * (2 * nraw + s); };
+  auto uempty = [&](int s) { return bar0 + 8u * (2 * nraw + nbr + s); };
+  const uint32_t bar1 = bar0 + 8u * (2 * nraw + 2 * nbr);
+  auto tfull = [&](int a) { return bar1 + 8u * a; };          // a < NB
+  auto tempty = [&](int a) { return bar1 + 8u * (4 + a); };
+  auto afull = [&](int c) { return bar1 + 8u * (8 + c); };    // c < 16 chunk slots
+  auto aempty = [&](int c) { return bar1 + 8u * (24 + c); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + (bar1 - sbase) + 8 * 40);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t kCols = 512;
+  const uint32_t a_col0 = NB * BN;
+
+  if (warp == 9) {
+    if (lane == 0) {
+      for (int s = 0; s < nraw; ++s) {
+        mbar_init(rfull(s), 1);
+        mbar_init(rempty(s), 256);
+      }
+      for (int s = 0; s < nbr; ++s) {
+        mbar_init(ufull(s), 1);
+        mbar_init(uempty(s), 1);
+      }
+      for (int a = 0; a < NB; ++a) {
+        mbar_init(tfull(a), 1);
+        mbar_init(tempty(a), 2);
+      }
+      for (int c = 0; c < n_chunks; ++c) {
+        mbar_init(afull(c), 2);
+        mbar_init(aempty(c), 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();
+  pdl_trigger();
+  const int sv = scale_exp(*vmax);
+  const float vscale = exp2i(-sv);
+  const float mscale = exp2i(sv) * __ldg(uscal);
+
+  const int n_mp = (T - t_lo + 2 * BM - 1) / (2 * BM);
+  const long long total = (long long)P * n_mp;
+  const long long u_beg = blockIdx.x >> 1, u_step = gridDim.x >> 1;
+  auto skip = [&](int nb, int c) { return (zmask >> (nb * 8 + c)) & 1; };
+
+  if (warp == 8) {
+    if (lane == 0) {  // ---------------- V producer: this CTA's 128 rows, once per unit
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long u = u_beg; u < total; u += u_step) {
+        const int xi = (int)(u / n_mp);
+        const int row0 = t_lo + (int)(u % n_mp) * 2 * BM + (int)rank * BM;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          mbar_wait(rempty(s), ph ^ 1u);
+          mbar_expect_tx(rfull(s), a_bytes);
+          if (l2hint) tma_load_3d_hint(raw0 + s * a_bytes, &tmA, row0, ch * KC, xi, rfull(s), l2_policy(false));
+          else tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * KC, xi, rfull(s));
+          if (++s == nraw) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ---------------- U producer: (n-block, chunk) pairs of the unit
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long u = u_beg; u < total; u += u_step) {
+        const int xi = (int)(u / n_mp);
+        for (int nb = 0; nb < NB; ++nb) {
+          const int col0 = nb * BN + (int)rank * HN;
+          for (int ch = 0; ch < n_chunks; ++ch) {
+            if (skip(nb, ch)) continue;
+            mbar_wait(uempty(s), ph ^ 1u);
+            const uint32_t st = ub0 + s * 2 * hb_bytes;
+            const uint32_t lb = mapa(ufull(s), 0);
+            if (leader) mbar_expect_tx(ufull(s), 4u * hb_bytes);
+            tma_load_3d_pair(st, &tmBhi, col0, ch * KC, xi, lb);
+            tma_load_3d_pair(st + hb_bytes, &tmBlo, col0, ch * KC, xi, lb);
+            if (++s == nbr) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (leader) {  // ---------------- MMA issuer (leader CTA)
+      constexpr uint32_t idesc = idesc_f16_pair<BN>();
+      constexpr uint32_t lbo = (uint32_t)KC * 128u;
+      int us = 0;
+      uint32_t uph = 0, uphase = 0;   // uphase: the unit's parity (A slots, accumulators)
+      for (long long u = u_beg; u < total; u += u_step) {
+        for (int nb = 0; nb < NB; ++nb) {
+          mbar_wait(tempty(nb), uphase ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem_base + nb * BN;
+          bool first = true;
+          for (int ch = 0; ch < n_chunks; ++ch) {
+            const bool sk = skip(nb, ch);
+            if (nb == 0) mbar_wait(afull(ch), uphase);
+            if (!sk) {
+              mbar_wait(ufull(us), uph);
+              tc_fence_after();
+              const uint32_t b_hi = ub0 + us * 2 * hb_bytes;
+              const uint64_t dh = sdesc_f16(b_hi, lbo), dl = sdesc_f16(b_hi + hb_bytes, lbo);
+              const uint32_t bhi32 = (uint32_t)(dh >> 32), bh = (uint32_t)dh, bl = (uint32_t)dl;
+              const uint32_t a_hi = tmem_base + a_col0 + ch * KC, a_lo = a_hi + KC / 2;
+              if (elect_one()) {
+#pragma unroll
+                for (int j = 0; j < NKS; ++j) {
+                  mma2_f16_split(d, a_lo + 8 * j, bh + 128 * j, bhi32, idesc, (first && j == 0) ? 0u : 1u);
+                  mma2_f16_split(d, a_hi + 8 * j, bl + 128 * j, bhi32, idesc, 1u);
+                  mma2_f16_split(d, a_hi + 8 * j, bh + 128 * j, bhi32, idesc, 1u);
+                }
+                tc2_commit_mc(uempty(us));
+              }
+              __syncwarp();
+              first = false;
+              if (++us == nbr) { us = 0; uph ^= 1u; }
+            }
+            if (nb == NB - 1) {   // last reader of chunk slot ch in this unit
+              if (elect_one()) tc2_commit_mc(aempty(ch));
+              __syncwarp();
+            }
+          }
+          if (elect_one()) tc2_commit_mc(tfull(nb));
+          __syncwarp();
+        }
+        uphase ^= 1u;
+      }
+    }
+  } else if (warp < 4 || (warp >= 11 && warp < 15)) {  // ---- converter (8 warps), each chunk once per unit
+    const int q = warp & 3, grp = warp < 4 ? 0 : 1;
+    const int row = q * 32 + lane;
+    const uint32_t lane_sel = (uint32_t)(q * 32) << 16;
+    constexpr int NG = KC / 16;
+    const int g0 = grp * NG / 2, g1 = (grp + 1) * NG / 2;
+    int rs = 0;
+    uint32_t rph = 0, uphase = 0;
+    for (long long u = u_beg; u < total; u += u_step) {
+      for (int ch = 0; ch < n_chunks; ++ch) {
+        mbar_wait(rfull(rs), rph);
+        mbar_wait(aempty(ch), uphase ^ 1u);
+        tc_fence_after();
+        const float* rawp = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
+        const uint32_t ahi = tmem_base + lane_sel + a_col0 + ch * KC;
+        for (int gg = g0; gg < g1; ++gg) {
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float v0 = rawp[(gg * 16 + 2 * j) * BM] * vscale;
+            const float v1 = rawp[(gg * 16 + 2 * j + 1) * BM] * vscale;
+            const __half2 h = __floats2half2_rn(v0, v1);
+            const float2 hf = __half22float2(h);
+            const __half2 l = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+            hi[j] = *reinterpret_cast<const uint32_t*>(&h);
+            lo[j] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          tmem_st8(ahi + gg * 8, hi);
+          tmem_st8(ahi + KC / 2 + gg * 8, lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(rempty(rs));
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (threadIdx.x == 0) mbar_arrive_cluster(mapa(afull(ch), 0));
+        if (++rs == nraw) { rs = 0; rph ^= 1u; }
+      }
+      uphase ^= 1u;
+    }
+  } else if (warp < 8) {  // warps 4-7 ------------------ epilogue: NB accumulators per unit
+    const int q = warp - 4;
+    const uint64_t pol = l2_policy(true);
+    uint32_t uphase = 0;
+    for (long long u = u_beg; u < total; u += u_step) {
+      const int xi = (int)(u / n_mp);
+      const int mp = (int)(u % n_mp);
+      const int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+      for (int nb = 0; nb < NB; ++nb) {
+        mbar_wait(tfull(nb), uphase);
+        tc_fence_after();
+        float* out = Mo + ((long long)xi * K + (long long)nb * BN) * T_s + t;
+        const int kr_all = K - nb * BN;
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + nb * BN;
+        uint32_t ra[32], rb[32];
+        tmem_ld32_nowait(ta, ra);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int cb = 0; cb < BN / 32; ++cb) {
+          uint32_t(&cur)[32] = (cb & 1) ? rb : ra;
+          uint32_t(&nxt)[32] = (cb & 1) ? ra : rb;
+          if (cb + 1 < BN / 32) tmem_ld32_nowait(ta + (cb + 1) * 32, nxt);
+          if (t < T) store_m32<true>(out + (long long)cb * 32 * T_s, cur, T_s, kr_all - cb * 32, l2hint, pol, mscale);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x == 128) mbar_arrive_cluster(mapa(tempty(nb), 0));
+      }
+      uphase ^= 1u;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 9) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kCols) : "memory");
+  }
+}
+
 }  // namespace
 }  // namespace tc
 
@@ -412,9 +662,65 @@ static cudaError_t launch_f16_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, c
                     P, (int)t_lo, (int)T, Ts, C, K, nraw, nbr, l2hint, vmax, uscal, f16_dbg(), gemm_nbfast());
 }
 
+// k_gemm_f16n (V block resident in TMEM across the two n-blocks)
+template <int KC>
+static cudaError_t launch_f16n_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16,
+                                  float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
+                                  const unsigned int* vmax, const float* uscal, int zmask, cudaStream_t s) {
+  constexpr int BN = 128, NB = 2;
+  int nraw, nbr;
+  size_t smem;
+  if (!f16_smem(KC, &nraw, &nbr, &smem)) return cudaErrorInvalidConfiguration;
+  auto kern = tc::k_gemm_f16n<BN, KC, NB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long units = (long long)P * ((T - t_lo + 2 * tc::BM - 1) / (2 * tc::BM));
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  static int max_pairs_dev[kMaxDevices][2] = {};
+  int& max_pairs = max_pairs_dev[dev][KC == 64 ? 1 : 0];
+  if (!max_pairs) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(tg.num_sms);
+    cfg.blockDim = dim3(tc::kThreadsTS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = tg.num_sms / 2;
+    max_pairs = n;
+  }
+  const long long pairs = max_pairs < units ? max_pairs : units;
+  if (pairs < 1) return cudaSuccess;
+  static int l2hint = -1;
+  if (l2hint < 0) {
+    const char* ev = getenv("WINO_L2_HINTS");
+    l2hint = ev ? (atoi(ev) != 0) : 1;
+  }
+  const long long Ts = T_s;
+  return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, tg.tmA_ts, tmBhi16, tmBlo16, Mo,
+                    P, (int)t_lo, (int)T, Ts, C, K, nraw, nbr, l2hint, vmax, uscal, zmask);
+}
+
+// The V-resident kernel applies to two 128-wide n-blocks (128 < K <= 256)
+// whose converted V block fits next to both accumulators in TMEM (C <= 256).
+bool f16n_applies(int C, int K, int kc) {
+  const int n_chunks = (C + kc - 1) / kc;
+  return K > 128 && K <= 256 && n_chunks * kc + 2 * 128 <= 512 && n_chunks <= 16;
+}
+
 cudaError_t launch_gemm_f16(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16, float* Mo,
                             int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K, const unsigned int* vmax,
-                            const float* uscal, cudaStream_t s) {
+                            const float* uscal, cudaStream_t s, int zmask, bool vres) {
+  if (vres && f16n_applies(C, K, tg.kc)) {
+    if (tg.kc == 64) return launch_f16n_kc<64>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s);
+    if (tg.kc == 32) return launch_f16n_kc<32>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s);
+  }
   if (tg.kc == 64) return launch_f16_kc<64>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, s);
   if (tg.kc == 32) return launch_f16_kc<32>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, s);
   return cudaErrorNotSupported;

@@ -83,9 +83,14 @@ cudaError_t launch_gemm_ts2(const TcGemm& tg, float* Mo, int P, int64_t t_lo, in
 // a3 with the 3xFP16 scaled split on kind::f16 (gemm_f16.cu), CTA pairs, BN 128
 bool f16_supported(int K, int kc);
 cudaError_t f16_encode_u(CUtensorMap* tm, const void* base, int64_t K_s, int C, int P, int kc);
+// vres: the V-resident kernel k_gemm_f16n where it applies (f16n_applies:
+// 128 < K <= 256, C <= 256); it honours zmask (bit nb*8 + c: U chunk
+// (n-block nb, k-chunk c) is zero and skipped).  Same products, same order
+// per output as k_gemm_f16p: bit-identical results.
+bool f16n_applies(int C, int K, int kc);
 cudaError_t launch_gemm_f16(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16, float* Mo,
                             int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K, const unsigned int* vmax,
-                            const float* uscal, cudaStream_t s);
+                            const float* uscal, cudaStream_t s, int zmask = 0, bool vres = true);
 // U (fp32) -> scaled fp16 hi / lo halves; *uscal = 2^su (mx: scratch word)
 cudaError_t launch_split16(const float* u32, int64_t n, unsigned int* mx, void* hi, void* lo, float* uscal,
                            cudaStream_t s);
@@ -105,6 +110,23 @@ cudaError_t launch_gemm_fold(const TcGemm& tg, int bn, int g, int MO, float* W, 
 bool output_fold_supported(int N, int alpha, int m, int F, int spec);
 cudaError_t launch_output_fold(int N, int alpha, int m, int F, int spec, const float* W, float* y, const KGeom& g,
                                const XfParams& xp, cudaStream_t s);
+// a5, filter-side fold: the same W from a plain batched GEMM.  By linearity
+//   W[xo][o][k][t] = sum_q A^T_F[o][q] sum_c V_{xo*Q+q}[c][t] U_{xo*Q+q}[c][k]
+//                  = sum_{(q,c)} V'[xo][(q,c)][t] U'[xo][(q,c)][(o,k)],
+//   U'[xo][(q,c)][(o,k)] = A^T_F[o][q] U_{xo*Q+q}[c][k],
+// where V' is V itself viewed as [P/Q][Q*C][T_s]: W = V' U' is one GEMM per
+// outer point xo with a Q*C-deep reduction and MO*K columns, written in W's
+// layout [P/Q][MO*K][T_s].  U' is computed by the filter transform (fp64,
+// one rounding), so A^T_F costs nothing per forward; the GEMM does MO x the
+// multiply-adds of the unfused one (the fold's zero coefficients included).
+constexpr int kMaxUFoldQ = 64, kMaxUFoldMO = 8;
+struct UFoldTab {
+  double coef[kMaxUFoldQ][kMaxUFoldMO];   // exact product of A^T entries, RNE to fp64
+  int Q, MO;
+};
+// U' [P/Q][Q*C][K_s'] (K_s' >= MO*K, = fp.K_s) from g; fp.P / fp.C / fp.K are the layer's
+cudaError_t launch_filter_ufold(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
+                                const UFoldTab& uf, cudaStream_t s);
 // rows [t_lo, T) of every point (t_lo a multiple of 4)
 cudaError_t launch_gemm_tc(const TcGemm& tg, float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
                            cudaStream_t s);

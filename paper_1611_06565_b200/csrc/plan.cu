@@ -225,6 +225,15 @@ struct wino_plan_s {
   // (gemm_fold.cu); the M buffer then holds W [P/Q * MO][K][T_s]
   int fold_F = 0, fold_Q = 1, fold_MO = 1, fold_bn = 0, fold_g = 0;
   FoldTab fold_tab{};
+  // a5 filter-side fold (kernels.h, UFoldTab): uf_F > 0 folds A^T of the
+  // uf_F innermost axes into U' at filter-transform time; the GEMM is then
+  // the plain batched GEMM of shape (gP, gC, gK) = (P/Q, Q*C, MO*K) writing W
+  int uf_F = 0;
+  UFoldTab uf_tab{};
+  int64_t gP = 0;
+  int gC = 0, gK = 0;
+  int zmask = 0;   // U' chunks that are zero by construction (skipped by the V-resident f16 GEMM)
+  bool f16n = true;   // 3xFP16: the V-resident kernel where it applies (WINO_F16N=0, dev knob: k_gemm_f16p)
   // 3xFP16 GEMM (gemm_f16.cu): U as scaled fp16 halves in ubuf (hi | lo |
   // tail: uscal, umax | fp32 staging of the filter transform), vmax: max|V|
   // word (a2 maxes it, the GEMM reads it, a4 clears it)
@@ -317,6 +326,71 @@ static void plan_fold(wino_plan_s* p) {
   p->fold_g = g;
 }
 
+// a5 filter-side fold depth F for a fused-kernel plan: WINO_UFOLD (dev knob)
+// else the measured default (0: off).
+static int ufold_default(int N, int a, int m, int C, int K) {
+  // F(2^3, 3^3), F = 1 (tools/ufold_bench.sh, tools/f16n_ab.sh, B200, ms per
+  // layer): c3 1.69 (epilogue fold F = 2, 3xTF32) -> 1.28 (GEMM 1.14 -> 0.57,
+  // a4 0.19 -> 0.31).  Not F(4^2, 3^2) (c2 0.102 -> 0.133: the 4x wider GEMM
+  // is tensor-bound) nor N = 4 (c5: only F >= 2 exists there, see below).
+  // An explicit WINO_FOLD (the epilogue-fold dev knob) turns this default off.
+  // Only where the folded GEMM (alpha C deep, m K wide) takes the 3xFP16
+  // scheme (auto_gemm_mode: both >= 128), as measured.
+  if (getenv("WINO_FOLD")) return 0;
+  if (a == 4 && m == 2 && N == 3 && a * C >= 128 && m * K >= 128) return 1;
+  return 0;
+}
+// F = 1 only: the fold lengthens each TMEM accumulation chain Q = alpha^F
+// times (Q*C terms per accumulator), and the tensor core's fp32 accumulation
+// error grows with it (measured, ragged c3-like layer, relL2 vs float64:
+// unfused / epilogue fold 3.9e-7, filter-side F = 1 6.1e-7 (3xFP16) / 1.0e-6
+// (3xTF32), F = 2 1.6e-6 / 2.9e-6, F(2^4,3^4) F = 3 4.2e-6 / 8.3e-6 --
+// BASELINE.json's 2e-6 budget holds only at F = 1).
+constexpr int kMaxUFoldF = 1;
+
+// coef[q][o] = prod_f A^T[o_f][q_f] over the F innermost axes (last axis fastest)
+static void fold_coefs(const Transforms& t, int F, UFoldTab& uf) {
+  const int a = t.a, m = t.m;
+  uf.Q = ipow(a, F);
+  uf.MO = ipow(m, F);
+  for (int q = 0; q < uf.Q; ++q)
+    for (int o = 0; o < uf.MO; ++o) {
+      RatOps ro;
+      Rat c{1, 1};
+      int qq = q, oo = o;
+      for (int f = 0; f < F; ++f) {
+        c = ro.mul(c, t.AT[oo % m][qq % a]);
+        qq /= a;
+        oo /= m;
+      }
+      uf.coef[q][o] = rat_to_f64(c);
+    }
+}
+
+// Zero U' chunks of the filter-side fold: bit nb * 8 + ch is set when every
+// column of n-block nb (width bn) has A^T_F[o][q] = 0 for the chunk's point q
+// (chunks of kc channels, C a multiple of kc so a chunk holds one q); an
+// n-block keeps at least one chunk.  WINO_UFOLD_SKIP=0 (dev knob): no skips.
+static int ufold_zmask(const wino_plan_s* p, int bn) {
+  const char* ev = getenv("WINO_UFOLD_SKIP");
+  if (ev && atoi(ev) == 0) return 0;
+  const int kc = p->tg.kc, n_chunks = p->gC / kc, nnb = (p->gK + bn - 1) / bn;
+  if (n_chunks > 8 || nnb > 4) return 0;
+  int mask = 0;
+  for (int nb = 0; nb < nnb; ++nb) {
+    int mnb = 0;
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      const int q = ch * kc / p->C;
+      bool zero = true;
+      for (int col = nb * bn; col < (nb + 1) * bn && col < p->gK; ++col)
+        if (p->uf_tab.coef[q][col / p->K] != 0.0) zero = false;
+      if (zero) mnb |= 1 << ch;
+    }
+    if (mnb != (1 << n_chunks) - 1) mask |= mnb << (nb * 8);
+  }
+  return mask;
+}
+
 // WINO_GEMM_AUTO's scheme for a fused-kernel plan: 3xTF32 unless the 3xFP16
 // split (twice the tensor rate) applies; WINO_GEMM_AUTO_MODE=3/4 overrides
 // (dev knob).  See fold_default / DESIGN.md for the measurements.
@@ -383,7 +457,25 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   p->N = N; p->m = m; p->r = r; p->a = a; p->C = C; p->K = K; p->batch = batch;
   p->mixed = mixed;
   p->m0 = m0; p->r0 = r0; p->a0 = a0;
-  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? auto_gemm_mode(N, a, m, C, K, mixed, fuse) : gemm_mode;
+  {
+    // a5 filter-side fold: tensor-core GEMMs only, single-(m, r) plans with
+    // the folded output kernels instantiated, no L2 chunking
+    int F = ufold_default(N, a, m, C, K);
+    if (const char* ev = getenv("WINO_UFOLD")) F = atoi(ev);
+    const bool tc_req = gemm_mode == WINO_GEMM_AUTO || gemm_mode == WINO_GEMM_3XTF32 || gemm_mode == WINO_GEMM_3XF16;
+    if (F >= 1 && F <= kMaxUFoldF && F < N && tc_req && !mixed && !(fuse & WINO_FUSE_L2_CHUNK) && ipow(a, F) <= kMaxUFoldQ &&
+        ipow(m, F) <= kMaxUFoldMO && output_fold_supported(N, a, m, F, spec)) {
+      p->uf_F = F;
+      fold_coefs(t, F, p->uf_tab);
+    }
+  }
+  {
+    const int Q = p->uf_F ? p->uf_tab.Q : 1, MO = p->uf_F ? p->uf_tab.MO : 1;
+    p->gP = (int64_t)a0 * ipow(a, N - 1) / Q;
+    p->gC = Q * C;
+    p->gK = MO * K;
+  }
+  p->gemm_mode = gemm_mode == WINO_GEMM_AUTO ? auto_gemm_mode(N, a, m, p->gC, p->gK, mixed, fuse) : gemm_mode;
   p->fuse = fuse;
   p->spec = spec;
   if (const char* ev = getenv("WINO_IN_TMA")) p->use_tma_in = atoi(ev) != 0;
@@ -406,8 +498,10 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   p->P = (int64_t)a0 * ipow(a, N - 1);
   p->f16 = p->gemm_mode == WINO_GEMM_3XF16;
   const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32 || p->f16;
-  const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
-  p->K_s = tc ? (K + bn - 1) / bn * bn : (K + 31) / 32 * 32;
+  // K stride of U (the GEMM's B operand; MO * K columns under the filter-side fold)
+  const int gK = p->gK;
+  const int bn = gK <= 32 ? 32 : gK <= 64 ? 64 : gK <= 128 ? 128 : 256;
+  p->K_s = tc ? (gK + bn - 1) / bn * bn : (gK + 31) / 32 * 32;
 
   // tables
   const FloatTables ft = to_tables(t), ft0 = to_tables(t0);
@@ -467,7 +561,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     const int64_t nslab_all = p->chunked ? p->chunk_slabs : (int64_t)batch * g.nbox0 * g.nbox1;
     plan_input_planes(g, nslab_all * C, nsm);
   }
-  const size_t ucount = (size_t)p->P * C * p->K_s;
+  const size_t ucount = (size_t)p->gP * p->gC * p->K_s;   // U, or U' under the filter-side fold
   const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
   p->filter_bytes = ucount * 4 * nbuf + (p->f16 ? 256 : 0);
   p->ws_bytes = ((size_t)p->P * C * p->T_s + (size_t)p->P * K * p->T_s) * 4;
@@ -517,19 +611,24 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     p->filter_bcast_bytes = ucount * 4 + 256;
   }
   if (tc) {
-    e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, (int)p->P, p->T_s, C, (int)p->K_s, K,
+    // the GEMM runs on (gP, gC, gK) = (P, C, K), or (P/Q, Q*C, MO*K) with V
+    // viewed as [P/Q][Q*C][T_s] under the filter-side fold
+    const int gP = (int)p->gP, gC = p->gC;
+    e = tc_gemm_prepare(p->tg, p->V, p->Uhi, p->Ulo, gP, p->T_s, gC, (int)p->K_s, gK,
                         p->gemm_mode == WINO_GEMM_1XTF32 ? 0 : 1, device);
     if (e == cudaSuccess && p->f16) {
-      if (p->chunked || !f16_supported(K, p->tg.kc)) {
+      if (p->chunked || !f16_supported(gK, p->tg.kc)) {
         wino_plan_destroy(p);
         return fail(WINO_ERR_UNSUPPORTED, "3xFP16 GEMM needs K > 64, a k-chunk of 32 or 64 (C >= 32) and no L2 chunking");
       }
-      e = f16_encode_u(&p->tmBhi16, p->U16hi, p->K_s, C, (int)p->P, p->tg.kc);
-      if (e == cudaSuccess) e = f16_encode_u(&p->tmBlo16, p->U16lo, p->K_s, C, (int)p->P, p->tg.kc);
+      e = f16_encode_u(&p->tmBhi16, p->U16hi, p->K_s, gC, gP, p->tg.kc);
+      if (e == cudaSuccess) e = f16_encode_u(&p->tmBlo16, p->U16lo, p->K_s, gC, gP, p->tg.kc);
+      if (const char* ev = getenv("WINO_F16N")) p->f16n = atoi(ev) != 0;
+      if (p->uf_F && p->f16n && C % p->tg.kc == 0 && f16n_applies(gC, gK, p->tg.kc)) p->zmask = ufold_zmask(p, 128);
     }
-    if (e == cudaSuccess && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32) plan_fold(p);
+    if (e == cudaSuccess && !p->uf_F && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32) plan_fold(p);
     if (e == cudaSuccess && !p->fold_F && !p->f16)
-      e = tc_gemm_tune(p->tg, p->M, (int)p->P, p->chunked ? p->T_s : T, p->T_s, C, K, p->V);
+      e = tc_gemm_tune(p->tg, p->M, gP, p->chunked ? p->T_s : T, p->T_s, gC, gK, p->V);
     if (e != cudaSuccess) {
       wino_plan_destroy(p);
       return fail(WINO_ERR_CUDA, "tcgen05 GEMM setup failed: %s", cudaGetErrorString(e));
@@ -628,6 +727,9 @@ static wino_status create_generic(wino_plan_t* plan_out, int N, const int64_t* d
   if (T > (int64_t)INT32_MAX - 256) { delete p; return fail(WINO_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)T); }
   p->T_s = (T + 127) / 128 * 128;
   p->P = P;
+  p->gP = P;
+  p->gC = C;
+  p->gK = K;
   if (P > 65535) { delete p; return fail(WINO_ERR_UNSUPPORTED, "prod alpha_n = %lld points exceeds 65535", (long long)P); }
   const bool tc = p->gemm_mode == WINO_GEMM_3XTF32 || p->gemm_mode == WINO_GEMM_1XTF32;
   const int bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
@@ -729,9 +831,12 @@ wino_status wino_filter_transform(wino_plan_t p, const float* g, wino_stream_t s
   CUDA_TRY(cudaGetLastError());
   if (p->f16) {
     // fp32 U (one rounding from fp64) into the staging area, then the scaled fp16 split
-    CUDA_TRY(launch_filter_xform(g, nullptr, nullptr, p->U32tmp, p->fp, (cudaStream_t)stream));
-    CUDA_TRY(launch_split16(p->U32tmp, (int64_t)p->P * p->C * p->K_s, p->umax, p->U16hi, p->U16lo, p->uscal,
+    if (p->uf_F) CUDA_TRY(launch_filter_ufold(g, nullptr, nullptr, p->U32tmp, p->fp, p->uf_tab, (cudaStream_t)stream));
+    else CUDA_TRY(launch_filter_xform(g, nullptr, nullptr, p->U32tmp, p->fp, (cudaStream_t)stream));
+    CUDA_TRY(launch_split16(p->U32tmp, p->gP * p->gC * p->K_s, p->umax, p->U16hi, p->U16lo, p->uscal,
                             (cudaStream_t)stream));
+  } else if (p->uf_F) {
+    CUDA_TRY(launch_filter_ufold(g, p->Uhi, p->Ulo, p->U32, p->fp, p->uf_tab, (cudaStream_t)stream));
   } else {
     CUDA_TRY(launch_filter_xform(g, p->Uhi, p->Ulo, p->U32, p->fp, (cudaStream_t)stream));
   }
@@ -840,21 +945,21 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
     if (p->f16) {
-      CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->P, t_lo - g.t0, t_hi - g.t0, p->T_s, p->C,
-                               p->K, p->vmax, p->uscal, s));
+      CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->gP, t_lo - g.t0, t_hi - g.t0, p->T_s,
+                               p->gC, p->gK, p->vmax, p->uscal, s, p->zmask, p->f16n));
     } else if (p->fold_F) {
       CUDA_TRY(launch_gemm_fold(p->tg, p->fold_bn, p->fold_g, p->fold_MO, p->M, (int)p->P, p->fold_Q, t_lo - g.t0,
                                 t_hi - g.t0, p->T_s, p->C, p->K, p->fold_tab, s));
     } else if (p->gemm_mode == WINO_GEMM_FFMA) {
       CUDA_TRY(launch_gemm_ffma(p->V, p->U32, p->M, (int)p->P, t_hi - g.t0, p->T_s, p->C, p->K, (int)p->K_s, s));
     } else {
-      CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->P, t_lo - g.t0, t_hi - g.t0, p->T_s, p->C, p->K, s));
+      CUDA_TRY(launch_gemm_tc(p->tg, p->M, (int)p->gP, t_lo - g.t0, t_hi - g.t0, p->T_s, p->gC, p->gK, s));
     }
     if (rec) CUDA_TRY(pg.end());
     ProfScope po{p, s, 2};
     if (rec) CUDA_TRY(po.begin());
-    if (p->fold_F) {
-      CUDA_TRY(launch_output_fold(p->N, p->a, p->m, p->fold_F, p->spec, p->M, y, g, p->xp, s));
+    if (p->fold_F || p->uf_F) {
+      CUDA_TRY(launch_output_fold(p->N, p->a, p->m, p->fold_F + p->uf_F, p->spec, p->M, y, g, p->xp, s));
     } else if (p->mixed) {
       CUDA_TRY(launch_output_mixed(p->N, p->a0, p->m0, p->a, p->m, p->M, y, g, p->xp,
                                    p->tm_M_ok ? &p->tm_M : nullptr, s));
@@ -954,11 +1059,12 @@ wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
   int64_t launches = 3;
   if (p->tiny) launches = 1;
   else if (p->chunked) launches = 3 * (((int64_t)p->batch * p->geom.nbox0 + p->chunk_slabs - 1) / p->chunk_slabs);
-  const int64_t v[24] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
+  const int64_t v[25] = {p->N, p->m, p->r, p->a, p->C, p->K, p->batch, p->Tps, p->T_s, p->P, p->K_s,
                          p->gemm_mode, p->fuse, p->tg.bn, p->tg.kc, p->chunked ? p->chunk_slabs : 0,
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
                          p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches,
-                         p->nd ? 0 : p->geom.nbox1, p->fold_F};
+                         p->nd ? 0 : p->geom.nbox1, p->fold_F + p->uf_F,
+                         p->uf_F ? 2 : p->fold_F ? 1 : 0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

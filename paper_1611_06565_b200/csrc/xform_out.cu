@@ -134,6 +134,55 @@ k_filter_xform_blk(const float* __restrict__ g, float* __restrict__ Uhi, float* 
   }
 }
 
+// a1 for the filter-side fold (kernels.h, UFoldTab): one thread per
+// (xo, (q, c), (o, k)), (o, k) fastest:
+//   U'[xo][q*C + c][o*K + k] = A^T_F[o][q] * sum_p prod_n G_n[xi_n][p_n] g[k, c, p],  xi = xo*Q + q
+// in fp64 (the sum as k_filter_xform), rounded once to fp32, then split.
+__global__ void __launch_bounds__(256)
+k_filter_ufold(const float* __restrict__ g, float* __restrict__ Uhi, float* __restrict__ Ulo,
+               float* __restrict__ U32, const __grid_constant__ FParams fp, const __grid_constant__ UFoldTab uf) {
+  const int64_t gC = (int64_t)uf.Q * fp.C;
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;   // (q*C + c) * K_s' + (o*K + k)
+  const int64_t xo = blockIdx.y;
+  if (i >= gC * fp.K_s) return;
+  const int ok = (int)(i % fp.K_s);
+  const int qc = (int)(i / fp.K_s);
+  const int q = qc / fp.C, c = qc - q * fp.C;
+  const int o = ok / fp.K, k = ok - o * fp.K;
+  float u = 0.f;
+  const double cf = o < uf.MO ? uf.coef[q][o] : 0.0;
+  if (cf != 0.0) {
+    int rN = 1;
+    for (int n = 0; n < fp.N; ++n) rN *= fp.r[n];
+    const float* gk = g + ((int64_t)k * fp.C + c) * rN;
+    int xd[kMaxN];
+    int64_t qq = xo * uf.Q + q;
+    for (int n = fp.N - 1; n >= 0; --n) { xd[n] = (int)(qq % fp.a[n]); qq /= fp.a[n]; }
+    double acc = 0.0;
+    for (int p = 0; p < rN; ++p) {
+      double w = 1.0;
+      int pq = p;
+      for (int n = fp.N - 1; n >= 0; --n) { w *= fp.G[n][xd[n]][pq % fp.r[n]]; pq /= fp.r[n]; }
+      if (w != 0.0) acc = fma(w, (double)__ldg(gk + p), acc);
+    }
+    u = (float)(cf * acc);
+  }
+  const int64_t at = xo * gC * fp.K_s + i;
+  const float hi = tf32_rna(u);
+  if (Uhi) Uhi[at] = hi;
+  if (Ulo) Ulo[at] = tf32_rna(u - hi);
+  if (U32) U32[at] = u;
+}
+
+cudaError_t launch_filter_ufold(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
+                                const UFoldTab& uf, cudaStream_t s) {
+  if (uf.Q < 1 || uf.MO < 1 || fp.P % uf.Q) return cudaErrorInvalidValue;
+  const int64_t n = (int64_t)uf.Q * fp.C * fp.K_s;
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)(fp.P / uf.Q));
+  k_filter_ufold<<<grid, 256, 0, s>>>(g, Uhi, Ulo, U32, fp, uf);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_filter_xform(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 cudaStream_t s) {
   int rN = 1;

@@ -213,7 +213,7 @@ def wino_plan_sizes(plan: int):
 
 INFO_KEYS = ["N", "m", "r", "alpha", "C", "K", "batch", "T_per_sample", "T_stride", "n_points", "K_stride",
              "gemm_mode", "fuse", "n_blk", "k_chunk", "chunk_slabs", "gemm_variant", "in_slab_tiles",
-             "in_planes_per_cta", "axis_mode", "tiny", "launches", "in_bands", "fold"]
+             "in_planes_per_cta", "axis_mode", "tiny", "launches", "in_bands", "fold", "fold_mode"]
 
 
 def wino_plan_info(plan: int) -> dict:

@@ -158,3 +158,21 @@ def test_per_axis_speedup_and_bytes():
     a = cost.stage_model(2, (56, 56), 4, 3, 128, 128, 32, (1, 1))
     b = cost.stage_model(2, (56, 56), (4, 4), (3, 3), 128, 128, 32, (1, 1))
     assert a == b
+
+
+def test_stage_model_fold_bytes():
+    # a5 folds: W = (m/alpha)^F of M; the filter-side fold
+    # (fold_mode 2) streams U' = m^F U and executes m^F x the multiply-adds
+    from paper_1611_06565_b200.cost import stage_model
+    args = (3, (16, 56, 56), 2, 3, 64, 128, 16, (1, 1, 1))
+    s0 = stage_model(*args)
+    T, P, C, K = s0["tiles"], 64, 64, 128
+    Vb, Mb, Ub = 4 * P * C * T, 4 * P * K * T, 4 * P * C * K
+    assert s0["gemm"]["bytes"] == Vb + Ub + Mb
+    s1 = stage_model(*args, fold=1, fold_mode=2)
+    assert s1["gemm"]["bytes"] == Vb + 2 * Ub + Mb // 2
+    assert s1["gemm"]["flops"] == 2 * s0["gemm"]["flops"]
+    assert s1["output_xform"]["bytes"] == s0["output_xform"]["bytes"] - Mb // 2
+    s2 = stage_model(*args, fold=2, fold_mode=1)
+    assert s2["gemm"]["bytes"] == Vb + Ub + Mb // 4 and s2["gemm"]["flops"] == s0["gemm"]["flops"]
+    assert s2["input_xform"] == s0["input_xform"]

@@ -83,8 +83,10 @@ def test_f16_unsupported_shapes_are_errors():
 
 
 def test_auto_scheme_choice():
-    # WINO_GEMM_AUTO: 3xFP16 where measured faster (C, K >= 128: c2, c4), 3xTF32 elsewhere
-    for name, want in (("c2", F16), ("c4", F16), ("c3", wino.WINO_GEMM_3XTF32), ("c5", wino.WINO_GEMM_3XTF32)):
+    # WINO_GEMM_AUTO: 3xFP16 where measured faster (GEMM depth and width >= 128:
+    # c2, c4, and c3 whose filter-side fold makes the GEMM 4 x 64 deep and
+    # 2 x 128 wide), 3xTF32 elsewhere
+    for name, want in (("c2", F16), ("c4", F16), ("c3", F16), ("c5", wino.WINO_GEMM_3XTF32)):
         cfg = CONFIGS[name]
         plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, 2, cfg.padding)
         assert plan.info["gemm_mode"] == want, (name, plan.info["gemm_mode"])
@@ -109,3 +111,29 @@ def test_f16_host_path_and_filter_broadcast():
     assert torch.equal(p2.forward(x.cuda()).cpu(), y)
     p1.close()
     p2.close()
+
+
+# K = 200 (two n-blocks, the second ragged), C = 256 (four 64-channel chunks):
+# the V-resident kernel (k_gemm_f16n) applies
+F16N = LayerConfig("f16d", 3, 2, 256, 200, (4, 9, 10), 3, 1, 4, "relu_normal", "he")
+
+
+@pytest.mark.parametrize("cfg", [F16N, SMALLF[1]], ids=lambda c: c.name)
+def test_f16_vresident_bit_identical(cfg, monkeypatch):
+    """k_gemm_f16n (V converted once per unit, kept in TMEM across the
+    n-blocks) issues the same MMAs in the same order per output as
+    k_gemm_f16p: bit-identical y; and within tolerance of the oracle."""
+    x, g = make_inputs(cfg)
+    ys = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("WINO_F16N", env)
+        plan = _plan(cfg)
+        plan.filter_transform(g.cuda())
+        ys.append(plan.forward(x.cuda()).cpu())
+        plan.close()
+    assert torch.equal(ys[0], ys[1])
+    ref = direct.direct_conv_f64(x.numpy(), g.numpy(), cfg.pad)
+    rel, mx = fm.errors(ys[0].double().numpy(), ref)
+    tl, tm = tolerance(cfg)
+    print("%s f16n relL2=%.3e max=%.3e" % (cfg.name, rel, mx))
+    assert rel <= tl and mx <= tm

@@ -126,13 +126,16 @@ def test_fold_stage_w(name, F, monkeypatch):
 
 
 def test_fold_off_where_infeasible_or_slower(monkeypatch):
-    # default plans: F = 2 for F(2^N, 3^N), N >= 3 (measured faster); no fold
-    # for F(4^N, 3^N), for small channel counts (k-chunk < 32) or chunked plans
+    # default plans: the epilogue fold F = 2 for F(2^4, 3^4) (measured
+    # faster); F(2^3, 3^3) takes the filter-side fold F = 1 instead
+    # (tests/test_gpu_ufold.py); no fold for F(4^N, 3^N), for small channel
+    # counts (k-chunk < 32) or chunked plans
     monkeypatch.delenv("WINO_FOLD", raising=False)
-    for name, want in (("c3", 2), ("c5", 2), ("c2", 0), ("c4", 0)):
+    monkeypatch.delenv("WINO_UFOLD", raising=False)
+    for name, want in (("c3", (1, 2)), ("c5", (2, 1)), ("c2", (0, 0)), ("c4", (0, 0))):
         cfg = CONFIGS[name]
         plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, 2, cfg.padding)
-        assert plan.info["fold"] == want, (name, plan.info["fold"])
+        assert (plan.info["fold"], plan.info["fold_mode"]) == want, (name, plan.info)
         plan.close()
     cfg = SMALL["c3"]                                   # C = 16: k-chunk 16
     plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, 2, cfg.padding)
