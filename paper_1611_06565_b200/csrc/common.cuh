@@ -72,6 +72,8 @@ struct KGeom {
   int in_threads;            // block size of the input kernel (<= 256; <= 512 in H mode)
   int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
   int in_flags;              // dev A/B knob of the input kernel (WINO_IN_FLAGS; 0 in production)
+  int in_pad8;               // in-place H mode, m = 4: phase-2 items on 8 axis-2 slots per row
+                             // (slots >= tiles[2] idle) so 8 lanes read 8 distinct 16-byte bank groups
   // 3xFP16 GEMM scaling (gemm_f16.cu): a2 atomically maxes |V| into *vmax,
   // a4 resets *vmax_reset = 0 for the next forward (NULL = not used)
   unsigned int* vmax;
@@ -111,6 +113,8 @@ template <int M_, int R_, int PS_>
 struct ConstTab {
   static constexpr bool kConst = true;
   static_assert(synthesize_default(M_, R_, PS_).err == 0, "default synthesis failed");
+  // the same tables as compile-time constants (structure detection, xform_common.cuh)
+  static constexpr FloatTables kTab = to_tables(synthesize_default(M_, R_, PS_));
   __device__ static __forceinline__ float bt(const XfParams&, int x, int i) { return kDevTab<M_, R_, PS_>.BT[x][i]; }
   __device__ static __forceinline__ float at(const XfParams&, int x, int i) { return kDevTab<M_, R_, PS_>.AT[x][i]; }
 };

@@ -100,6 +100,7 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   }
   g.in_flags = 0;
   if (const char* ev = getenv("WINO_IN_FLAGS")) g.in_flags = atoi(ev);  // dev A/B knob
+  g.in_pad8 = 0;
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;
   g.smem_bytes = (int)(g.slot_bytes + hb);
@@ -131,6 +132,26 @@ void plan_input_planes(KGeom& g, int64_t nwork, int num_sms) {
   if (npl > kMaxPlanes) npl = kMaxPlanes;
   if (!pooled) npl = 1;
   g.npl = npl;
+  // in-place H mode with m = 4: phase-2 items on 8 slots per axis-1 row
+  // (conflict-free 128-bit window loads; the wide tail load of the last real
+  // tile stays inside the row), block size with the fewest idle item slots
+  // in the last round (WINO_IN_PAD8=0, dev knob: dense items)
+  const char* ev_p8 = getenv("WINO_IN_PAD8");
+  const int tl2 = g.tiles[2];
+  if (g.hinplace && g.m % 4 == 0 && g.e[0] > 1 && tl2 % 8 && (tl2 - 1) * g.m + 8 <= g.pitch &&
+      (!ev_p8 || atoi(ev_p8) != 0)) {
+    g.in_pad8 = 1;
+    if (!getenv("WINO_IN_THREADS")) {
+      const int64_t items = (int64_t)g.e[0] * npl * g.bt1 * ((tl2 + 7) / 8 * 8);   // alpha_0 (bt0 = 1) x slots
+      int best = g.in_threads;
+      int64_t waste = (items + best - 1) / best * best - items;
+      for (int t = 256; t <= 512; t += 32) {
+        const int64_t w = (items + t - 1) / t * t - items;
+        if (w < waste) { waste = w; best = t; }
+      }
+      g.in_threads = best;
+    }
+  }
   g.smem_bytes = npl * g.slot_bytes + (pooled ? 0 : (g.smem_bytes - g.slot_bytes));
 }
 

@@ -71,6 +71,22 @@ __device__ __forceinline__ void load_row(const float* p, float* r) {
   load_seg<cap, D, D + A>(p, r);
 }
 
+// A window values of one 16-byte aligned row with ceil(A/4) 128-bit loads
+// (the tail load reads up to 3 floats past the window; the caller keeps them
+// inside the row).  Lanes whose rows start at consecutive 16-byte groups then
+// hit 8 distinct bank groups per quarter warp on every load.
+template <int A>
+__device__ __forceinline__ void load_row_wide(const float* p, float* r) {
+#pragma unroll
+  for (int q = 0; q < (A + 3) / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(p + 4 * q);
+    if (4 * q + 0 < A) r[4 * q + 0] = v.x;
+    if (4 * q + 1 < A) r[4 * q + 1] = v.y;
+    if (4 * q + 2 < A) r[4 * q + 2] = v.z;
+    if (4 * q + 3 < A) r[4 * q + 3] = v.w;
+  }
+}
+
 // Axis-0 transform of a plan: F(M0, .) with alpha_0 = A0 and table Tab0.
 // Equal to the other axes' (A, M, Tab) for the usual single-(m, r) plans; a
 // different one for the per-axis plans with a distinct axis 0 (e.g. F(2,3)
@@ -319,19 +335,10 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           for (int i = 0; i < A0; ++i) v[i] = act ? row[xh + D + i * g.sst[0]] : 0.f;
           __syncwarp();  // all reads of this pass before any shifted write
           if (act) {
+            float w[A0];
+            xform_line<A0, A0, Get0>(v, w, xp);
 #pragma unroll
-            for (int x0 = 0; x0 < A0; ++x0) {
-              float acc = 0.f;
-              bool first = true;
-#pragma unroll
-              for (int i = 0; i < A0; ++i) {
-                if (Get0::nz(xp, x0, i)) {
-                  acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
-                  first = false;
-                }
-              }
-              row[xh + x0 * g.sst[0]] = acc;
-            }
+            for (int x0 = 0; x0 < A0; ++x0) row[xh + x0 * g.sst[0]] = w[x0];
           }
           __syncwarp();  // writes of this pass before the next pass's reads
         }
@@ -343,44 +350,62 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // phase 2: one work item per (xi_0, plane, t1, t2) on plane xi_0 of its
       // slab; xi_0 outermost, so a round of the block writes long runs of t
       // (npl planes are adjacent in t) into each of the alpha^2 planes of V
-      // it touches (measured: the V store pattern bounds this kernel)
-      const int R = tl1 * tl2, nrun = npl * R;
+      // it touches (measured: the V store pattern bounds this kernel).
+      // g.in_pad8: t2 runs over 8 slots per row (m = 4: window starts 16 bytes
+      // apart, so the 8 lanes of a quarter warp read 8 distinct bank groups;
+      // slots >= tl2 idle) -- no shared-memory bank conflicts
+      const int tl2p = g.in_pad8 ? (tl2 + 7) / 8 * 8 : tl2;
+      const int R = tl1 * tl2p, nrun = npl * R;
       // item u = ((xi0 * npl + p) * tl1 + t1) * tl2 + t2, stepped by the block
       // size with mixed-radix carries (three run-time divisions per item
       // otherwise); the step's digits are computed once
       const int ustep = blockDim.x;
-      const int st2 = ustep % tl2, st1 = (ustep / tl2) % tl1, stp = (ustep / R) % npl, sxi = ustep / nrun;
+      const int st2 = ustep % tl2p, st1 = (ustep / tl2p) % tl1, stp = (ustep / R) % npl, sxi = ustep / nrun;
       int xi0, p, t1, t2;
       {
         const int u0 = threadIdx.x;
         xi0 = u0 / nrun;
         p = (u0 / R) % npl;
-        t1 = (u0 / tl2) % tl1;
-        t2 = u0 % tl2;
+        t1 = (u0 / tl2p) % tl1;
+        t2 = u0 % tl2p;
       }
       for (int u = threadIdx.x; u < A0 * nrun; u += ustep) {
         if (g.in_flags & 1) {   // dev A/B: the plain divisions
           xi0 = u / nrun;
           p = (u / R) % npl;
-          t1 = (u / tl2) % tl1;
-          t2 = u % tl2;
+          t1 = (u / tl2p) % tl1;
+          t2 = u % tl2p;
         }
-        const int tl = t1 * tl2 + t2;
-        const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
-        float h[A * A];
-        if constexpr (A0 == 1) ensure(p);
-        constexpr int DS = A0 > 1 ? 0 : D;  // shifted by phase 1, else at the TMA offset
+        if (t2 < tl2) {
+          const int tl = t1 * tl2 + t2;
+          const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
+          float h[A * A];
+          if constexpr (A0 == 1) ensure(p);
+          constexpr int DS = A0 > 1 ? 0 : D;  // shifted by phase 1, else at the TMA offset
+          if constexpr (DS == 0 && M % 4 == 0) {
+            if (g.in_pad8) {
 #pragma unroll
-        for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
-        all_axes<A, 2, A, A, Get>(h, xp);
-        float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
+              for (int i1 = 0; i1 < A; ++i1) load_row_wide<A>(hp0 + i1 * g.sst[1], h + i1 * A);
+            } else {
 #pragma unroll
-        for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
-        vtrack<A * A>(g, h, vm);
+              for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
+            }
+          } else {
+#pragma unroll
+            for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
+          }
+          all_axes<A, 2, A, A, Get>(h, xp);
+          float* vo = vbase(p) + tl + (int64_t)xi0 * (A * A) * pstride;
+          if (!(g.in_flags & 4)) {   // (dev probe, in_flags & 4: no V stores; results invalid)
+#pragma unroll
+            for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
+          }
+          vtrack<A * A>(g, h, vm);
+        }
         // next item: add the step digit by digit (t2 fastest)
         t2 += st2;
-        int cy = t2 >= tl2;
-        t2 -= cy ? tl2 : 0;
+        int cy = t2 >= tl2p;
+        t2 -= cy ? tl2p : 0;
         t1 += st1 + cy;
         cy = t1 >= tl1;
         t1 -= cy ? tl1 : 0;
@@ -405,19 +430,10 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
 #pragma unroll
         for (int i = 0; i < A0; ++i) v[i] = col[i * g.sst[0]];
         float* hrow = H + (t0l * A0 * e1 + y) * hp + xh;
+        float w[A0];
+        xform_line<A0, A0, Get0>(v, w, xp);
 #pragma unroll
-        for (int x0 = 0; x0 < A0; ++x0) {
-          float acc = 0.f;
-          bool first = true;
-#pragma unroll
-          for (int i = 0; i < A0; ++i) {
-            if (Get0::nz(xp, x0, i)) {
-              acc = first ? Get0::v(xp, x0, i) * v[i] : fmaf(Get0::v(xp, x0, i), v[i], acc);
-              first = false;
-            }
-          }
-          hrow[x0 * e1 * hp] = acc;
-        }
+        for (int x0 = 0; x0 < A0; ++x0) hrow[x0 * e1 * hp] = w[x0];
       }
     }
     __syncthreads();
