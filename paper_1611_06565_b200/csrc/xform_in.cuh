@@ -323,6 +323,49 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // run-time division per row was a fifth of this pass's instructions)
       int p = 0, y = warp;
       while (y >= e1) { y -= e1; ++p; }
+      if (g.in_flags & 8) {   // (dev probe, in_flags & 8: staging only -- wait for the slabs, no transform)
+        ensure(npl - 1);
+        return;
+      }
+      if (e2 <= 32 && !(g.in_flags & 2)) {
+        // one pass per row: two rows per iteration (their loads issued
+        // together), one warp sync between a row pair's reads and its shifted
+        // writes; rows are private to the warp, so no sync between pairs
+        const int sst0 = g.sst[0], sst1 = g.sst[1], nrows = npl * e1;
+        const bool act = lane < e2;
+        for (int r = warp; r < nrows; r += 2 * nwarps) {
+          int p2 = p, y2 = y + nwarps;
+          while (y2 >= e1) { y2 -= e1; ++p2; }
+          const bool two = r + nwarps < nrows;
+          ensure(two ? p2 : p);
+          float* c1 = S0 + p * slab_f + y * sst1 + lane;
+          float* c2 = S0 + p2 * slab_f + y2 * sst1 + lane;
+          float v1[A0], v2[A0];
+          if (act) {
+#pragma unroll
+            for (int i = 0; i < A0; ++i) v1[i] = c1[D + i * sst0];
+            if (two) {
+#pragma unroll
+              for (int i = 0; i < A0; ++i) v2[i] = c2[D + i * sst0];
+            }
+          }
+          __syncwarp();  // all reads of the pair before any shifted write
+          if (act) {
+            float w[A0];
+            xform_line<A0, A0, Get0>(v1, w, xp);
+#pragma unroll
+            for (int x0 = 0; x0 < A0; ++x0) c1[x0 * sst0] = w[x0];
+            if (two) {
+              xform_line<A0, A0, Get0>(v2, w, xp);
+#pragma unroll
+              for (int x0 = 0; x0 < A0; ++x0) c2[x0 * sst0] = w[x0];
+            }
+          }
+          p = p2;
+          y = y2 + nwarps;
+          while (y >= e1) { y -= e1; ++p; }
+        }
+      } else
       for (int r = warp; r < npl * e1; r += nwarps) {
         if (g.in_flags & 2) { p = r / e1; y = r - p * e1; }   // dev A/B: the plain division
         ensure(p);
