@@ -91,6 +91,57 @@ __host__ __device__ constexpr bool has_mirror_rows() {
     if (mirror_row<Get, A, R>(x) >= 0) return true;
   return false;
 }
+// Mirrored row pairs regardless of their length (row y > x of a constant
+// table with cv(y, i) == (-1)^i cv(x, i)): an a2 work item that combines the
+// slab rows along axis 0 for output point x can produce y from the same row
+// loads (xform_in.cuh).  -1: none, or x is itself the mirror of a row.
+template <class Get, int A>
+__host__ __device__ constexpr int mirror_any(int x) {
+  if constexpr (!Get::kConst) {
+    return -1;
+  } else {
+    for (int z = 0; z < x; ++z) {   // x already taken as the mirror of z
+      bool ok = true;
+      for (int i = 0; i < A; ++i) {
+        const float a = Get::cv(z, i), b = Get::cv(x, i);
+        if (b != ((i & 1) ? -a : a)) ok = false;
+      }
+      if (ok) return -1;
+    }
+    for (int y = x + 1; y < A; ++y) {
+      bool ok = true, used = false;
+      for (int i = 0; i < A; ++i) {
+        const float a = Get::cv(x, i), b = Get::cv(y, i);
+        if (b != ((i & 1) ? -a : a)) ok = false;
+        if (a != 0.f) used = true;
+      }
+      if (ok && used) return y;
+    }
+    return -1;
+  }
+}
+template <class Get, int A>
+__host__ __device__ constexpr bool is_mirror_any(int y) {
+  for (int x = 0; x < y; ++x)
+    if (mirror_any<Get, A>(x) == y) return true;
+  return false;
+}
+// work-item kinds along axis 0: every output point that is not the mirror of
+// an earlier one (a kind with a mirror produces both points)
+template <class Get, int A>
+__host__ __device__ constexpr int mirror_kinds() {
+  int n = 0;
+  for (int x = 0; x < A; ++x)
+    if (!is_mirror_any<Get, A>(x)) ++n;
+  return n;
+}
+template <class Get, int A>
+__host__ __device__ constexpr int kind_point(int k) {
+  for (int x = 0; x < A; ++x)
+    if (!is_mirror_any<Get, A>(x) && k-- == 0) return x;
+  return -1;
+}
+
 // One line: out[x] = sum_i Get(x, i) in[i] for x < R (in and out may not
 // alias).  Constant tables with mirrored rows take the shared partial sums;
 // otherwise one FMA chain per output, zero terms skipped.

@@ -114,8 +114,11 @@ __device__ __forceinline__ void vtrack(const KGeom& g, const float* h, float& vm
 }
 
 // One work item: axis-0 output point X0 of one tile whose window starts at
-// slab offset `base` (+ D columns); writes alpha^(N-1) values of V.
-template <int N, int A, int M, class Tab, int D, int X0, class Ax>
+// slab offset `base` (+ D columns); writes alpha^(N-1) values of V.  Y0 >= 0:
+// also the mirrored point Y0 (B^T[Y0][i] = (-1)^i B^T[X0][i]) from the same
+// slab-row loads: the even- and odd-i0 partial sums e, o give X0 = e + o and
+// Y0 = e - o (half the shared-memory reads of two separate items).
+template <int N, int A, int M, class Tab, int D, int X0, class Ax, int Y0 = -1>
 __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, const KGeom& g,
                                         const XfParams& xp, float* __restrict__ vout, int64_t pstride, float& vm) {
   using Get = BTget<Tab>;
@@ -137,6 +140,47 @@ __device__ __forceinline__ void in_work(const float* __restrict__ S, int base, c
 #pragma unroll
     for (int j = 0; j < A * A; ++j) vput(vout + j * pstride, h[j], vm);
     vtrack<A * A>(g, h, vm);
+  } else if constexpr (Y0 >= 0) {
+    constexpr int NL = N - 1;
+    constexpr int P1 = ipow(A, NL);
+    constexpr int ROWS = ipow(A, NL - 1);
+    float e[P1], o[P1];
+#pragma unroll
+    for (int j = 0; j < P1; ++j) { e[j] = 0.f; o[j] = 0.f; }
+    bool fe = true, fo = true;
+    sfor<0, Ax::A>([&](auto I0) {
+      constexpr int i0 = decltype(I0)::value;
+      constexpr float bv = Get0::cv(X0, i0);
+      if constexpr (bv != 0.f) {
+        float* h = (i0 & 1) ? o : e;
+        const bool first = (i0 & 1) ? fo : fe;
+#pragma unroll
+        for (int rw = 0; rw < ROWS; ++rw) {
+          int off = base + i0 * g.sst[0];
+#pragma unroll
+          for (int ax = 1; ax < N - 1; ++ax) off += ((rw / ipow(A, N - 2 - ax)) % A) * g.sst[ax];
+          float r[A];
+          load_row<A, M, D>(S + off, r);
+#pragma unroll
+          for (int i = 0; i < A; ++i) h[rw * A + i] = first ? bv * r[i] : fmaf(bv, r[i], h[rw * A + i]);
+        }
+        if (i0 & 1) fo = false; else fe = false;
+      }
+    });
+#pragma unroll
+    for (int j = 0; j < P1; ++j) {
+      const float t = e[j];
+      e[j] = t + o[j];
+      o[j] = t - o[j];
+    }
+    all_axes<A, NL, A, A, Get>(e, xp);
+#pragma unroll
+    for (int j = 0; j < P1; ++j) vput(vout + (X0 * P1 + j) * pstride, e[j], vm);
+    vtrack<P1>(g, e, vm);
+    all_axes<A, NL, A, A, Get>(o, xp);
+#pragma unroll
+    for (int j = 0; j < P1; ++j) vput(vout + (Y0 * P1 + j) * pstride, o[j], vm);
+    vtrack<P1>(g, o, vm);
   } else {
     constexpr int NL = N - 1;            // axes handled in registers
     constexpr int P1 = ipow(A, NL);      // values per work item
@@ -175,6 +219,34 @@ __device__ __forceinline__ void in_dispatch(int xi0, const float* S, int base, c
   if constexpr (X0 < Ax::A) {
     if (xi0 == X0) in_work<N, A, M, Tab, D, X0, Ax>(S, base, g, xp, vout, pstride, vm);
     else in_dispatch<N, A, M, Tab, D, Ax, X0 + 1>(xi0, S, base, g, xp, vout, pstride, vm);
+  }
+}
+
+// Axis-0 work-item kinds of the combination path (N >= 3, or a distinct axis
+// 0): with a constant table, one kind per output point that is not the
+// mirror of an earlier one (xform_common.cuh mirror_any); a kind with a
+// mirror writes both points.  Run tables: one kind per point.  Only where a
+// pair item's two register sets stay small (2 alpha^(N-1) <= 32: F(2^3,3^3)
+// measured 0.339 -> 0.322 ms on c3's input; F(2^4,3^4) with 2 x 64 values
+// per item was slower, c5 61 -> 70 us).
+template <int N, int A, class Ax>
+constexpr bool in_pairs() { return 2 * ipow(A, N - 1) <= 32; }
+template <int N, int A, class Ax>
+constexpr int in_kinds() { return in_pairs<N, A, Ax>() ? mirror_kinds<BTget<typename Ax::Tab>, Ax::A>() : Ax::A; }
+
+template <int N, int A, int M, class Tab, int D, class Ax, int K = 0>
+__device__ __forceinline__ void in_dispatch_kind(int kind, const float* S, int base, const KGeom& g,
+                                                 const XfParams& xp, float* vout, int64_t pstride, float& vm) {
+  if constexpr (K < in_kinds<N, A, Ax>()) {
+    if (kind == K) {
+      using Get0 = BTget<typename Ax::Tab>;
+      constexpr bool pairs = in_pairs<N, A, Ax>();
+      constexpr int x0 = pairs ? kind_point<Get0, Ax::A>(K) : K;
+      constexpr int y0 = pairs ? mirror_any<Get0, Ax::A>(x0) : -1;
+      in_work<N, A, M, Tab, D, x0, Ax, y0>(S, base, g, xp, vout, pstride, vm);
+    } else {
+      in_dispatch_kind<N, A, M, Tab, D, Ax, K + 1>(kind, S, base, g, xp, vout, pstride, vm);
+    }
   }
 }
 
@@ -545,7 +617,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     // ---- work items (plane, xi_0, tile), tile fastest
     // work items per tile: one per xi_0 when N >= 3 or when axis 0 has its
     // own transform (N = 2 per-axis plans); one whole tile otherwise
-    constexpr int NX = (N >= 3 || Ax::A != A || Ax::M != M) ? Ax::A : 1;
+    constexpr bool kComb = N >= 3 || Ax::A != A || Ax::M != M;   // axis-0 combination items
+    constexpr int NX = kComb ? in_kinds<N, A, Ax>() : 1;
     if (npl == 1) {
       // one plane: no plane index to decode (the common case for large slabs)
       ensure(0);
@@ -563,7 +636,8 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
           base += ti * M * g.sst[ax];
         }
         base += rem * Ax::M * g.sst[0];
-        in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride, vm);
+        if constexpr (kComb) in_dispatch_kind<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride, vm);
+        else in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0, base, g, xp, vb + tl, pstride, vm);
       }
       return;
     }
@@ -586,7 +660,10 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         base += ti * M * g.sst[ax];
       }
       base += rem * Ax::M * g.sst[0];
-      in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride, vm);
+      if constexpr (kComb)
+        in_dispatch_kind<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride, vm);
+      else
+        in_dispatch<N, A, M, Tab, D, Ax>(xi0, S0 + p * slab_f, base, g, xp, vbase(p) + tl, pstride, vm);
     }
   }
 }
