@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include <type_traits>
 #include <utility>
@@ -145,7 +146,41 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// Launch `kern` with the PDL attribute on stream s.
+// WINO_PDL=0 (dev knob): plain stream-ordered launches (griddepcontrol is a
+// no-op without the attribute)
+// WINO_PDL_MASK (dev knob): PDL only for the stages whose bit is set (1
+// input transform, 2 GEMM, 4 output transform; the plan tags the stage it
+// launches through pdl_stage())
+inline int& pdl_cur_stage() {
+  static thread_local int st = 0;
+  return st;
+}
+inline void pdl_stage(int s) { pdl_cur_stage() = s; }
+inline bool pdl_enabled() {
+  static int on = -1, mask = 7;
+  if (on < 0) {
+    const char* ev = getenv("WINO_PDL");
+    on = ev ? (atoi(ev) != 0) : 1;
+    if (const char* em = getenv("WINO_PDL_MASK")) mask = atoi(em);
+  }
+  const int st = pdl_cur_stage();
+  return on != 0 && (st == 0 || (mask >> (st - 1)) & 1);
+}
+
+// Launch `kern` with the PDL attribute on stream s (unless `pdl` is false:
+// plain stream order).  Grids of more than kPdlMaxCtasPerSm CTAs per SM are
+// launched without it (pdl_grid_ok): launched early behind the GEMM, c3's
+// 100k-CTA output grid made the layer 5% slower (1.27 vs 1.20 ms), while the
+// 6k-CTA c2 and 2k-CTA c5 output grids gain from the overlap.
+constexpr int kPdlMaxCtasPerSm = 64;
+inline bool pdl_grid_ok(long long ctas) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  static int sms_dev[kMaxDevices] = {};
+  if (!sms_dev[dev] && cudaDeviceGetAttribute(&sms_dev[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms_dev[dev] = 148;
+  return ctas <= (long long)kPdlMaxCtasPerSm * sms_dev[dev];
+}
 template <class... KArgs, class... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -158,7 +193,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() && pdl_grid_ok((long long)grid.x * grid.y * grid.z) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -936,6 +936,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     g.T = t_hi;
     ProfScope ps{p, s, 0};
     if (rec) CUDA_TRY(ps.begin());
+    pdl_stage(1);
     if (p->mixed) {
       CUDA_TRY(launch_input_mixed(p->N, p->a0, p->m0, p->a, p->m, x, p->V, g, p->xp, tm, (int)(s1 - s0), s));
     } else {
@@ -944,6 +945,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(ps.end());
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
+    pdl_stage(2);
     if (p->f16) {
       CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->gP, t_lo - g.t0, t_hi - g.t0, p->T_s,
                                p->gC, p->gK, p->vmax, p->uscal, s, p->zmask, p->f16n));
@@ -958,6 +960,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     if (rec) CUDA_TRY(pg.end());
     ProfScope po{p, s, 2};
     if (rec) CUDA_TRY(po.begin());
+    pdl_stage(3);
     if (p->fold_F || p->uf_F) {
       CUDA_TRY(launch_output_fold(p->N, p->a, p->m, p->fold_F + p->uf_F, p->spec, p->M, y, g, p->xp, s));
     } else if (p->mixed) {
@@ -967,6 +970,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
       CUDA_TRY(launch_output_xform(p->N, p->a, p->m, p->spec, p->M, y, g, p->xp, p->tm_M_ok ? &p->tm_M : nullptr, s));
     }
     if (rec) CUDA_TRY(po.end());
+    pdl_stage(0);
   }
   if (rec) ++p->prof_calls;
   return WINO_OK;
