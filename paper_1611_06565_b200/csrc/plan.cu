@@ -643,7 +643,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     // shards of a tiny layer take the same path (reading #8)
     int TB, smem;
     const char* ev = getenv("WINO_TINY");
-    p->tiny = (ev && atoi(ev) != 0) && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32 &&
+    p->tiny = (ev && atoi(ev) != 0) && !mixed && !p->chunked && !p->uf_F && p->gemm_mode == WINO_GEMM_3XTF32 &&
               tiny_supported(N, a, m) && tiny_shape(N, a, C, K, p->P, &TB, &smem) && p->P * Tps * (int64_t)C <= 8192 &&
               K <= 64;
   }
