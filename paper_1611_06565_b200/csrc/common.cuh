@@ -79,6 +79,7 @@ struct KGeom {
   // a4 resets *vmax_reset = 0 for the next forward (NULL = not used)
   unsigned int* vmax;
   unsigned int* vmax_reset;
+  unsigned long long* trace;   // dev probe (WINO_IN_TRACE): per-CTA %globaltimer events of a2 (NULL in production)
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

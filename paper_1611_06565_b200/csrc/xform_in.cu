@@ -1,5 +1,6 @@
 // xform_in.cu -- host side of stage a2: slab geometry, the TMA descriptor of
 // x, and dispatch to the instantiations (xform_in_const.cu, xform_in_run.cu).
+#include <cstdio>
 #include <cstdlib>
 
 #include "tma.hpp"
@@ -180,10 +181,38 @@ bool encode_input_map(CUtensorMap* tm, const float* x, const KGeom& g, int N, in
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
-                               const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s) {
+static cudaError_t launch_input_xform1(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
+                                       const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s) {
   if (spec != kSpecRuntime) return launch_input_const(N, alpha, m, spec, x, V, g, xp, tm, nslab, s);
   return launch_input_run(N, alpha, m, x, V, g, xp, tm, nslab, s);
+}
+
+// dev probe (WINO_IN_TRACE=<file>): every a2 launch records, per CTA, its SM
+// and the %globaltimer at start / slabs landed / axis-0 pass done / end
+// (H mode in place), and the last launch's records are written to <file>
+// (one line per CTA).  The launch is synchronised; results stay valid.
+cudaError_t launch_input_xform(int N, int alpha, int m, int spec, const float* x, float* V, const KGeom& g,
+                               const XfParams& xp, const CUtensorMap* tm, int nslab, cudaStream_t s) {
+  const char* path = getenv("WINO_IN_TRACE");
+  if (!path) return launch_input_xform1(N, alpha, m, spec, x, V, g, xp, tm, nslab, s);
+  const long long grid = ((long long)nslab * g.C + g.npl - 1) / g.npl;
+  const size_t bytes = (size_t)grid * 8 * sizeof(unsigned long long);
+  KGeom g1 = g;
+  cudaError_t e = cudaMalloc(&g1.trace, bytes);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(g1.trace, 0, bytes, s);
+  e = launch_input_xform1(N, alpha, m, spec, x, V, g1, xp, tm, nslab, s);
+  cudaStreamSynchronize(s);
+  unsigned long long* h = (unsigned long long*)malloc(bytes);
+  cudaMemcpy(h, g1.trace, bytes, cudaMemcpyDeviceToHost);
+  if (FILE* f = fopen(path, "w")) {
+    for (long long b = 0; b < grid; ++b)
+      fprintf(f, "%llu %llu %llu %llu %llu\n", h[b * 8], h[b * 8 + 1], h[b * 8 + 2], h[b * 8 + 3], h[b * 8 + 4]);
+    fclose(f);
+  }
+  free(h);
+  cudaFree(g1.trace);
+  return e;
 }
 
 }  // namespace wino

@@ -98,6 +98,20 @@ struct Ax0 {
   using Tab = Tab0_;
 };
 
+// dev probe (g.trace): %globaltimer of CTA event ev
+__device__ __forceinline__ void in_trace(const KGeom& g, int ev) {
+  if (g.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g.trace[(size_t)blockIdx.x * 8 + ev] = t;
+    if (ev == 1) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      g.trace[(size_t)blockIdx.x * 8] = sm;
+    }
+  }
+}
+
 __device__ __forceinline__ void vput(float* p, float v, float& vm) {
   (void)vm;
   *p = v;
@@ -395,6 +409,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // run-time division per row was a fifth of this pass's instructions)
       int p = 0, y = warp;
       while (y >= e1) { y -= e1; ++p; }
+      if (g.trace && threadIdx.x == 0) { ensure(npl - 1); in_trace(g, 2); }
       if (g.in_flags & 8) {   // (dev probe, in_flags & 8: staging only -- wait for the slabs, no transform)
         ensure(npl - 1);
         return;
@@ -462,6 +477,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       }
       }
       __syncthreads();
+      in_trace(g, 3);
       // phase 2: one work item per (xi_0, plane, t1, t2) on plane xi_0 of its
       // slab; xi_0 outermost, so a round of the block writes long runs of t
       // (npl planes are adjacent in t) into each of the alpha^2 planes of V
@@ -692,31 +708,43 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   const int nwork = nslab * g.C;
   const int w0 = blockIdx.x * g.npl;
   const int npl = min(g.npl, nwork - w0);
+  // slab indices of one launch fit 32 bits (nwork is an int): unsigned
+  // divisions here -- the int64 ones, five plane decodes in a row on thread
+  // 0 ahead of the TMA issue, held the whole block at the first barrier
+  // (ncu: 18% of the c4 kernel's warp samples on that barrier)
   auto plane = [&](int w) {
     PlaneInfo q;
-    const int64_t slab = g.s_beg + w % nslab;    // ((b * nbox0 + box0) * nbox1 + box1)
-    q.c = w / nslab;
-    const int64_t s0 = slab / g.nbox1;
-    q.a1 = (int)(slab - s0 * g.nbox1) * g.bt1;
-    q.b = (int)(s0 / g.nbox0);
-    const int box = (int)(s0 - (int64_t)q.b * g.nbox0);
+    const unsigned slab = (unsigned)(g.s_beg + (unsigned)w % (unsigned)nslab);   // ((b * nbox0 + box0) * nbox1 + box1)
+    q.c = (int)((unsigned)w / (unsigned)nslab);
+    const unsigned s0 = slab / (unsigned)g.nbox1;
+    q.a1 = (int)(slab - s0 * (unsigned)g.nbox1) * g.bt1;
+    q.b = (int)(s0 / (unsigned)g.nbox0);
+    const int box = (int)(s0 - (unsigned)q.b * (unsigned)g.nbox0);
     q.a0 = box * g.bt0;
     q.nt0 = min(g.bt0, g.tiles[0] - q.a0);
     return q;
   };
-  if (threadIdx.x < npl) pl[threadIdx.x] = plane(w0 + threadIdx.x);
+  PlaneInfo mine{};
+  if (threadIdx.x < npl) {
+    mine = plane(w0 + threadIdx.x);
+    pl[threadIdx.x] = mine;
+  }
   pdl_wait();      // x may come from the preceding kernel; V is read by the previous GEMM
   pdl_trigger();
+  in_trace(g, 1);
   if constexpr (kTma) {
     static_assert(N >= 2, "TMA slab path needs N >= 2");
     const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+    // lane 0 initialises the slab barriers, then lane p (< npl <= 8, all in
+    // warp 0) issues slab p's box
     if (threadIdx.x == 0) {
       for (int p = 0; p < npl; ++p) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8u * p) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int p = 0; p < npl; ++p) {
-        const PlaneInfo q = plane(w0 + p);
-        issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, q.b, q.a0, q.c, q.a1 * M, mb0 + 8u * p);
-      }
+    }
+    if (threadIdx.x < 32) __syncwarp();
+    if (threadIdx.x < npl) {
+      const int p = threadIdx.x;
+      issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, mine.b, mine.a0, mine.c, mine.a1 * M, mb0 + 8u * p);
     }
     __syncthreads();
   } else {
@@ -730,6 +758,10 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
   float vm = 0.f;
   transform_planes<N, A, M, Tab, D, Ax>(smem_f, slab_f, H, V, g, xp, pl, npl,
                                     kTma ? (uint32_t)__cvta_generic_to_shared(&bar[0]) : 0u, vm);
+  if (g.trace) {
+    __syncthreads();
+    in_trace(g, 4);
+  }
   // max|V| of the whole launch (the 3xFP16 GEMM's scale): block reduction,
   // one atomicMax per CTA (non-negative floats order as their bit patterns)
   if (g.vmax) {
