@@ -155,15 +155,15 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int n_mp = (T - t_lo + 2 * BM - 1) / (2 * BM);
   const int n_nblk = (K + BN - 1) / BN;
-  const long long per_xi = (long long)n_nblk * n_mp;
-  const long long total = (long long)P * per_xi;
-  const long long u_beg = blockIdx.x >> 1, u_step = gridDim.x >> 1;
+  const unsigned per_xi = (unsigned)n_nblk * (unsigned)n_mp;   // units fit 32 bits (32-bit decode)
+  const unsigned total = (unsigned)P * per_xi;
+  const unsigned u_beg = blockIdx.x >> 1, u_step = gridDim.x >> 1;
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- V producer: this CTA's 128 rows
       int s = 0;
       uint32_t ph = 0;
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / per_xi);
         const int mp = nbfast ? (int)(u % per_xi) / n_nblk : (int)(u % per_xi) % n_mp;
         const int row0 = t_lo + mp * 2 * BM + (int)rank * BM;
@@ -180,7 +180,7 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) {  // ---------------- U producer: this CTA's 64 columns (hi, lo)
       int s = 0;
       uint32_t ph = 0;
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / per_xi);
         const int nb = nbfast ? (int)(u % per_xi) % n_nblk : (int)(u % per_xi) / n_mp;
         const int col0 = nb * BN + (int)rank * HN;
@@ -201,7 +201,7 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       constexpr uint32_t lbo = (uint32_t)KC * 128u;
       int as = 0, us = 0;
       uint32_t aph = 0, uph = 0, acc = 0, cph = 0;
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         mbar_wait(tempty(acc), cph ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -240,7 +240,7 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int g0 = grp * NG / 2, g1 = (grp + 1) * NG / 2;
     int rs = 0, as = 0;
     uint32_t rph = 0, aph = 0;
-    for (long long u = u_beg; u < total; u += u_step) {
+    for (unsigned u = u_beg; u < total; u += u_step) {
       for (int ch = 0; ch < n_chunks; ++ch) {
         mbar_wait(rfull(rs), rph);
         mbar_wait(aempty(as), aph ^ 1u);
@@ -278,7 +278,7 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t tempty_l[4] = {mapa(tempty(0), 0), mapa(tempty(1), 0), mapa(tempty(2), 0), mapa(tempty(3), 0)};
     const uint64_t pol = l2_policy(true);
     uint32_t acc = 0, aph = 0;
-    for (long long u = u_beg; u < total; u += u_step) {
+    for (unsigned u = u_beg; u < total; u += u_step) {
       const int xi = (int)(u / per_xi);
       const int rr = (int)(u % per_xi);
       const int nb = nbfast ? rr % n_nblk : rr / n_mp, mp = nbfast ? rr / n_nblk : rr % n_mp;
@@ -403,15 +403,15 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const float mscale = exp2i(sv) * __ldg(uscal);
 
   const int n_mp = (T - t_lo + 2 * BM - 1) / (2 * BM);
-  const long long total = (long long)P * n_mp;
-  const long long u_beg = blockIdx.x >> 1, u_step = gridDim.x >> 1;
+  const unsigned total = (unsigned)P * (unsigned)n_mp;   // units fit 32 bits (32-bit decode)
+  const unsigned u_beg = blockIdx.x >> 1, u_step = gridDim.x >> 1;
   auto skip = [&](int nb, int c) { return (zmask >> (nb * 8 + c)) & 1; };
 
   if (warp == 8) {
     if (lane == 0) {  // ---------------- V producer: this CTA's 128 rows, once per unit
       int s = 0;
       uint32_t ph = 0;
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / n_mp);
         const int row0 = t_lo + (int)(u % n_mp) * 2 * BM + (int)rank * BM;
         for (int ch = 0; ch < n_chunks; ++ch) {
@@ -427,7 +427,7 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) {  // ---------------- U producer: (n-block, chunk) pairs of the unit
       int s = 0;
       uint32_t ph = 0;
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / n_mp);
         for (int nb = 0; nb < NB; ++nb) {
           const int col0 = nb * BN + (int)rank * HN;
@@ -450,7 +450,7 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       constexpr uint32_t lbo = (uint32_t)KC * 128u;
       int us = 0;
       uint32_t uph = 0, uphase = 0;   // uphase: the unit's parity (A slots, accumulators)
-      for (long long u = u_beg; u < total; u += u_step) {
+      for (unsigned u = u_beg; u < total; u += u_step) {
         for (int nb = 0; nb < NB; ++nb) {
           mbar_wait(tempty(nb), uphase ^ 1u);
           tc_fence_after();
@@ -498,7 +498,7 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int g0 = grp * NG / 2, g1 = (grp + 1) * NG / 2;
     int rs = 0;
     uint32_t rph = 0, uphase = 0;
-    for (long long u = u_beg; u < total; u += u_step) {
+    for (unsigned u = u_beg; u < total; u += u_step) {
       for (int ch = 0; ch < n_chunks; ++ch) {
         mbar_wait(rfull(rs), rph);
         mbar_wait(aempty(ch), uphase ^ 1u);
@@ -533,7 +533,7 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int q = warp - 4;
     const uint64_t pol = l2_policy(true);
     uint32_t uphase = 0;
-    for (long long u = u_beg; u < total; u += u_step) {
+    for (unsigned u = u_beg; u < total; u += u_step) {
       const int xi = (int)(u / n_mp);
       const int mp = (int)(u % n_mp);
       const int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
@@ -629,6 +629,7 @@ static cudaError_t launch_f16_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, c
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long units = (long long)P * ((K + BN - 1) / BN) * ((T - t_lo + 2 * tc::BM - 1) / (2 * tc::BM));
+  if (units >= (1LL << 31)) return cudaErrorNotSupported;   // the kernel decodes units in 32 bits
   // co-resident CTA pairs (occupancy query, as the tf32 pair kernel)
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
@@ -675,6 +676,7 @@ static cudaError_t launch_f16n_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long units = (long long)P * ((T - t_lo + 2 * tc::BM - 1) / (2 * tc::BM));
+  if (units >= (1LL << 31)) return cudaErrorNotSupported;   // the kernel decodes units in 32 bits
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
   static int max_pairs_dev[kMaxDevices][2] = {};
