@@ -262,6 +262,19 @@ def test_input_cp_async_fallback_matches_tma(name, monkeypatch):
     assert torch.equal(y_tma, y_cp)
 
 
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_input_slabs_per_cta_bit_identical(name, monkeypatch):
+    # a2's slabs per CTA (npl; the last CTA takes the ragged remainder, each
+    # slab's TMA box issued by its own lane of warp 0) and its block size only
+    # regroup work items: every V element is computed by the same operations,
+    # so the output bits must not change
+    cfg = SMALL[name]
+    y0, info0 = _run_env(cfg, monkeypatch)
+    for npl, thr in (("1", "256"), ("3", "320"), ("5", "256"), ("8", "448")):
+        y1, info1 = _run_env(cfg, monkeypatch, WINO_IN_NPL=npl, WINO_IN_THREADS=thr)
+        assert torch.equal(y0, y1), "npl=%s threads=%s (planned %d)" % (npl, thr, info1["in_planes_per_cta"])
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_output_tma_ring_matches_plain(name, monkeypatch):
     # a4 reading M through the TMA ring (alpha^(N-1) >= 32) and through plain
