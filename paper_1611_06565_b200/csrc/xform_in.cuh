@@ -112,9 +112,22 @@ __device__ __forceinline__ void in_trace(const KGeom& g, int ev) {
   }
 }
 
+// V store flavour (dev A/B builds, tools/build_variant.sh): 0 plain (default),
+// 1 st.cs (streaming), 2 st.cg, 3 st.wt
+#ifndef WINO_VPUT_MODE
+#define WINO_VPUT_MODE 0
+#endif
 __device__ __forceinline__ void vput(float* p, float v, float& vm) {
   (void)vm;
+#if WINO_VPUT_MODE == 1
+  __stcs(p, v);
+#elif WINO_VPUT_MODE == 2
+  __stcg(p, v);
+#elif WINO_VPUT_MODE == 3
+  __stwt(p, v);
+#else
   *p = v;
+#endif
 }
 // max|V| of the stored values for the 3xFP16 GEMM's scale (g.vmax set): one
 // uniform test per work item, the FMNMX only in such plans (a per-store max
