@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-I", str(CSRC), "-I", str(INCLUDE)]
 SOURCES = ["plan.cu", "xform_in.cu", "xform_in_const.cu", "xform_in_run.cu", "xform_in_run8.cu", "xform_out.cu", "xform_out_const.cu",
-           "xform_out_run.cu", "xform_nd.cu", "xform_mixed.cu", "xform_tiny.cu", "xform_fold.cu", "gemm_tc.cu", "gemm_ts2.cu", "gemm_fold.cu", "gemm_f16.cu",
+           "xform_out_run.cu", "xform_nd.cu", "xform_mixed.cu", "xform_tiny.cu", "xform_fold.cu", "xform_dfold.cu", "gemm_tc.cu", "gemm_ts2.cu", "gemm_fold.cu", "gemm_f16.cu",
            "gemm_ffma.cu"]
 
 

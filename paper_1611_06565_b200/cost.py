@@ -122,7 +122,12 @@ def stage_model(N: int, dims: Sequence[int], m, r, C: int, K: int, B: int,
     fold = F > 0 (a5, single (m, r)): the GEMM writes W, (m/alpha)^F of M's
     size, and a4 reads W.  fold_mode 2 (the filter-side fold) reads U' = m^F
     x U and executes m^F x the multiply-adds (zero coefficients included);
-    fold_mode 1 (epilogue fold) keeps U and the flops."""
+    fold_mode 1 (epilogue fold) keeps U and the flops.  fold_mode 3 (the
+    direct-axis fold, F = 1): a2 writes and the GEMM reads Z -- the input
+    transformed along the outer axes only, (m t + alpha - m) raw columns per
+    row of t tiles of the last axis -- instead of V, U' = m x U as in mode 2,
+    and the GEMM executes the last axis directly: m r / alpha x the
+    multiply-adds."""
     pad = tuple(pad) if pad is not None else (0,) * N
     mv = tuple(m) if isinstance(m, (list, tuple)) else (m,) * N
     rv = tuple(r) if isinstance(r, (list, tuple)) else (r,) * N
@@ -141,6 +146,13 @@ def stage_model(N: int, dims: Sequence[int], m, r, C: int, K: int, B: int,
         if fold_mode == 2:
             Ub *= mm ** fold                          # U'
             gflops *= mm ** fold
+        elif fold_mode == 3:
+            if fold != 1:
+                raise ValueError("the direct-axis fold is F = 1")
+            tl = -(-out[-1] // mm)                    # tiles along the last axis
+            Vb = 4 * (P // a) * C * (T // tl) * (mm * tl + a - mm)      # Z
+            Ub *= mm
+            gflops = gflops * mm * rv[0] // a
     st = {
         "filter_xform": {"bytes": 4 * K * C * math.prod(rv) + Ub, "flops": 0},
         "input_xform": {"bytes": xb + Vb, "flops": 0},

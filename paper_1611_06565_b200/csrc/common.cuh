@@ -80,6 +80,10 @@ struct KGeom {
   unsigned int* vmax;
   unsigned int* vmax_reset;
   unsigned long long* trace;   // dev probe (WINO_IN_TRACE): per-CTA %globaltimer events of a2 (NULL in production)
+  // a5 direct-axis fold (xform_dfold.cu): a2 transforms the outer axes only and
+  // writes Z [P/alpha * 2][C][Tz] (32-slot rows) instead of V
+  int dfold;
+  int64_t Tz;                  // slot pitch of a Z plane
 };
 
 // Runtime transform tables (generic path); constant-bank resident.

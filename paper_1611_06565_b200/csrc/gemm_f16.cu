@@ -329,12 +329,20 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // the epilogue while the MMAs of the next n-block run.  zmask bit nb*8 + c:
 // U chunk (nb, c) is zero by construction (filter-side fold, A^T_F[o][q] = 0
 // for every column of the n-block), its U load and MMAs are skipped.
-template <int BN, int KC, int NB>
+// DF (direct-axis fold, xform_dfold.cu): the A operand is Z [P*2][df_cz][Tz]
+// in 32-slot rows; k-chunk ch holds tap j = ch*KC / df_cz (df_cz a multiple of
+// KC), loaded as the {BM + 4, KC} box of plane xi*2 + (j & 1) at the unit's
+// 16-byte aligned first slot (TMA start coordinates must be 16-byte aligned:
+// tools/tma_off_probe.cu) and read by the converter at slot + (j >> 1); T
+// counts slots, and the epilogue stores slot (row, i < df_tl2) at tile
+// row * df_tl2 + i of W (a warp's 32 TMEM lanes are one row).
+template <int BN, int KC, int NB, bool DF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
 k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
             const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
             int C, int K, int nraw, int nbr, int l2hint, const unsigned int* __restrict__ vmax,
-            const float* __restrict__ uscal, int zmask) {
+            const float* __restrict__ uscal, int zmask, int df_tl2, int df_cz) {
+  constexpr int BMR = DF ? BM + 4 : BM;   // raw-stage row pitch (slots)
   constexpr int HN = BN / 2;
   static_assert(HN == 64, "one 64-wide fp16 swizzle group per CTA half");
   constexpr int NKS = KC / 16;
@@ -346,10 +354,10 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int n_chunks = (C + KC - 1) / KC;            // <= (512 - NB * BN) / KC (host-checked)
-  const uint32_t a_bytes = (uint32_t)BM * KC * 4;
+  const uint32_t a_bytes = (uint32_t)BMR * KC * 4;
   const uint32_t hb_bytes = (uint32_t)HN * KC * 2;
   const uint32_t raw0 = sbase;
-  const uint32_t ub0 = raw0 + nraw * a_bytes;
+  const uint32_t ub0 = (raw0 + nraw * a_bytes + 1023u) & ~1023u;   // (DF: a_bytes is not a multiple of 1024)
   const uint32_t bar0 = ub0 + 2u * nbr * hb_bytes;
   auto rfull = [&](int s) { return bar0 + 8u * s; };
   auto rempty = [&](int s) { return bar0 + 8u * (nraw + s); };
@@ -414,11 +422,20 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       for (unsigned u = u_beg; u < total; u += u_step) {
         const int xi = (int)(u / n_mp);
         const int row0 = t_lo + (int)(u % n_mp) * 2 * BM + (int)rank * BM;
-        for (int ch = 0; ch < n_chunks; ++ch) {
+        // DF: one box per (parity plane, channel chunk) -- taps j and j + 2
+        // read the same box at slots + 0 / + 1 (2 * df_cz / KC loads per unit)
+        const int n_loads = DF ? 2 * (df_cz / KC) : n_chunks;
+        for (int ch = 0; ch < n_loads; ++ch) {
           mbar_wait(rempty(s), ph ^ 1u);
           mbar_expect_tx(rfull(s), a_bytes);
-          if (l2hint) tma_load_3d_hint(raw0 + s * a_bytes, &tmA, row0, ch * KC, xi, rfull(s), l2_policy(false));
-          else tma_load_3d(raw0 + s * a_bytes, &tmA, row0, ch * KC, xi, rfull(s));
+          int crow = ch * KC, plane = xi;
+          if constexpr (DF) {
+            const int par = crow / df_cz;
+            crow -= par * df_cz;
+            plane = xi * 2 + par;
+          }
+          if (l2hint) tma_load_3d_hint(raw0 + s * a_bytes, &tmA, row0, crow, plane, rfull(s), l2_policy(false));
+          else tma_load_3d(raw0 + s * a_bytes, &tmA, row0, crow, plane, rfull(s));
           if (++s == nraw) { s = 0; ph ^= 1u; }
         }
       }
@@ -498,19 +515,29 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int g0 = grp * NG / 2, g1 = (grp + 1) * NG / 2;
     int rs = 0;
     uint32_t rph = 0, uphase = 0;
+    unsigned ld0 = 0;   // DF: raw loads issued before this unit (stage of load L: (ld0 + L) % nraw)
+    const int ncz = DF ? df_cz / KC : 1;
     for (unsigned u = u_beg; u < total; u += u_step) {
       for (int ch = 0; ch < n_chunks; ++ch) {
+        int tap = 0;
+        if constexpr (DF) {   // chunk (tap j, cc) reads load (j & 1, cc), filled once per unit
+          tap = ch / ncz;
+          const unsigned ld = ld0 + (unsigned)((tap & 1) * ncz + (ch - tap * ncz));
+          rs = (int)(ld % (unsigned)nraw);
+          rph = (ld / (unsigned)nraw) & 1u;
+        }
         mbar_wait(rfull(rs), rph);
         mbar_wait(aempty(ch), uphase ^ 1u);
         tc_fence_after();
         const float* rawp = reinterpret_cast<const float*>(smem + rs * a_bytes) + row;
+        if constexpr (DF) rawp += tap >> 1;   // tap j's slot shift
         const uint32_t ahi = tmem_base + lane_sel + a_col0 + ch * KC;
         for (int gg = g0; gg < g1; ++gg) {
           uint32_t hi[8], lo[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float v0 = rawp[(gg * 16 + 2 * j) * BM] * vscale;
-            const float v1 = rawp[(gg * 16 + 2 * j + 1) * BM] * vscale;
+            const float v0 = rawp[(gg * 16 + 2 * j) * BMR] * vscale;
+            const float v1 = rawp[(gg * 16 + 2 * j + 1) * BMR] * vscale;
             const __half2 h = __floats2half2_rn(v0, v1);
             const float2 hf = __half22float2(h);
             const __half2 l = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
@@ -522,11 +549,18 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
-        mbar_arrive(rempty(rs));
+        if constexpr (DF) {
+          if (tap >= 2) mbar_arrive(rempty(rs));   // the box's second and last reader
+        } else {
+          mbar_arrive(rempty(rs));
+        }
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (threadIdx.x == 0) mbar_arrive_cluster(mapa(afull(ch), 0));
-        if (++rs == nraw) { rs = 0; rph ^= 1u; }
+        if constexpr (!DF) {
+          if (++rs == nraw) { rs = 0; rph ^= 1u; }
+        }
       }
+      if constexpr (DF) ld0 += 2u * (unsigned)ncz;
       uphase ^= 1u;
     }
   } else if (warp < 8) {  // warps 4-7 ------------------ epilogue: NB accumulators per unit
@@ -536,7 +570,12 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (unsigned u = u_beg; u < total; u += u_step) {
       const int xi = (int)(u / n_mp);
       const int mp = (int)(u % n_mp);
-      const int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+      int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+      bool live = t < T;
+      if constexpr (DF) {   // slot (row, lane) -> tile row * tl2 + lane; slots >= tl2 of a row are padding
+        live = live && lane < df_tl2;
+        t = (t >> 5) * df_tl2 + lane;
+      }
       for (int nb = 0; nb < NB; ++nb) {
         mbar_wait(tfull(nb), uphase);
         tc_fence_after();
@@ -551,7 +590,7 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           uint32_t(&cur)[32] = (cb & 1) ? rb : ra;
           uint32_t(&nxt)[32] = (cb & 1) ? ra : rb;
           if (cb + 1 < BN / 32) tmem_ld32_nowait(ta + (cb + 1) * 32, nxt);
-          if (t < T) store_m32<true>(out + (long long)cb * 32 * T_s, cur, T_s, kr_all - cb * 32, l2hint, pol, mscale);
+          if (live) store_m32<true>(out + (long long)cb * 32 * T_s, cur, T_s, kr_all - cb * 32, l2hint, pol, mscale);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
@@ -573,10 +612,10 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 }  // namespace tc
 
 // ---------------------------------------------------------------- host side
-static bool f16_smem(int kc, int* nraw, int* nbr, size_t* bytes) {
-  const size_t a = (size_t)tc::BM * kc * 4;
+static bool f16_smem(int kc, int* nraw, int* nbr, size_t* bytes, int raw_rows = tc::BM) {
+  const size_t a = (size_t)raw_rows * kc * 4;   // (BM + 4 rows under the direct-axis fold)
   const size_t hb2 = 2ull * 64 * kc * 2;     // hi + lo halves of one chunk, fp16
-  const size_t fixed = 1024 + 1024;
+  const size_t fixed = 1024 + 1024 + (raw_rows != tc::BM ? 1024 : 0);   // + the U ring's 1 KB alignment
   const size_t budget = 232448;
   size_t left = budget - fixed;
   int nb = 4;
@@ -664,15 +703,17 @@ static cudaError_t launch_f16_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, c
 }
 
 // k_gemm_f16n (V block resident in TMEM across the two n-blocks)
-template <int KC>
+template <int KC, bool DF>
 static cudaError_t launch_f16n_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16,
                                   float* Mo, int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K,
-                                  const unsigned int* vmax, const float* uscal, int zmask, cudaStream_t s) {
+                                  const unsigned int* vmax, const float* uscal, int zmask, cudaStream_t s,
+                                  const DFoldGemm* df) {
   constexpr int BN = 128, NB = 2;
   int nraw, nbr;
   size_t smem;
-  if (!f16_smem(KC, &nraw, &nbr, &smem)) return cudaErrorInvalidConfiguration;
-  auto kern = tc::k_gemm_f16n<BN, KC, NB>;
+  if (!f16_smem(KC, &nraw, &nbr, &smem, DF ? tc::BM + 4 : tc::BM)) return cudaErrorInvalidConfiguration;
+  if (DF && nraw < 2 * (df->cz / KC)) return cudaErrorInvalidConfiguration;   // a unit's boxes are held together
+  auto kern = tc::k_gemm_f16n<BN, KC, NB, DF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long units = (long long)P * ((T - t_lo + 2 * tc::BM - 1) / (2 * tc::BM));
@@ -705,8 +746,23 @@ static cudaError_t launch_f16n_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, 
     l2hint = ev ? (atoi(ev) != 0) : 1;
   }
   const long long Ts = T_s;
-  return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, tg.tmA_ts, tmBhi16, tmBlo16, Mo,
-                    P, (int)t_lo, (int)T, Ts, C, K, nraw, nbr, l2hint, vmax, uscal, zmask);
+  return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, DF ? *df->tmA : tg.tmA_ts, tmBhi16,
+                    tmBlo16, Mo, P, (int)t_lo, (int)T, Ts, C, K, nraw, nbr, l2hint, vmax, uscal, zmask, DF ? df->tl2 : 0,
+                    DF ? df->cz : 0);
+}
+
+// Z of the direct-axis fold as (slot, c, plane): box {BM + 4, kc, 1}, no swizzle, zero fill past Tz
+cudaError_t f16_encode_z(CUtensorMap* tm, const float* Z, int64_t Tz, int cz, int planes, int kc) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {(cuuint64_t)Tz, (cuuint64_t)cz, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)Tz * 4, (cuuint64_t)Tz * 4 * cz};
+  cuuint32_t box[3] = {(cuuint32_t)tc::BM + 4, (cuuint32_t)kc, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(Z), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 // The V-resident kernel applies to two 128-wide n-blocks (128 < K <= 256)
@@ -718,10 +774,16 @@ bool f16n_applies(int C, int K, int kc) {
 
 cudaError_t launch_gemm_f16(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16, float* Mo,
                             int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K, const unsigned int* vmax,
-                            const float* uscal, cudaStream_t s, int zmask, bool vres) {
+                            const float* uscal, cudaStream_t s, int zmask, bool vres, const DFoldGemm* df) {
+  if (df) {   // direct-axis fold: the V-resident kernel only (the plan checked f16n_applies)
+    if (!f16n_applies(C, K, tg.kc) || df->cz % tg.kc != 0 || t_lo != 0) return cudaErrorNotSupported;
+    if (tg.kc == 64) return launch_f16n_kc<64, true>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s, df);
+    if (tg.kc == 32) return launch_f16n_kc<32, true>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s, df);
+    return cudaErrorNotSupported;
+  }
   if (vres && f16n_applies(C, K, tg.kc)) {
-    if (tg.kc == 64) return launch_f16n_kc<64>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s);
-    if (tg.kc == 32) return launch_f16n_kc<32>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s);
+    if (tg.kc == 64) return launch_f16n_kc<64, false>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s, nullptr);
+    if (tg.kc == 32) return launch_f16n_kc<32, false>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, zmask, s, nullptr);
   }
   if (tg.kc == 64) return launch_f16_kc<64>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, s);
   if (tg.kc == 32) return launch_f16_kc<32>(tg, tmBhi16, tmBlo16, Mo, P, t_lo, T, T_s, C, K, vmax, uscal, s);

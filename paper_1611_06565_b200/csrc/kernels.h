@@ -88,9 +88,22 @@ cudaError_t f16_encode_u(CUtensorMap* tm, const void* base, int64_t K_s, int C, 
 // (n-block nb, k-chunk c) is zero and skipped).  Same products, same order
 // per output as k_gemm_f16p: bit-identical results.
 bool f16n_applies(int C, int K, int kc);
+// df (direct-axis fold, xform_dfold.cu; V-resident kernel only): the A operand
+// is Z [P*2][cz][Tz] -- k-chunk (tap j, channels c0..) of unit (xo, 256-slot
+// block) is the box of plane xo*2 + (j & 1) at slot + (j >> 1) (loaded from
+// the 16-byte aligned slot, the shift applied by the converter); T counts
+// slots (rows * 32) and the epilogue stores slot (row, i < tl2) at tile
+// row * tl2 + i of W.
+struct DFoldGemm {
+  const CUtensorMap* tmA;   // Z as (slot, c, plane), box {132, kc, 1}, no swizzle (f16_encode_z)
+  int tl2;                  // tiles along the last axis (<= 31)
+  int cz;                   // layer channels C (a multiple of the k-chunk)
+};
+cudaError_t f16_encode_z(CUtensorMap* tm, const float* Z, int64_t Tz, int cz, int planes, int kc);
 cudaError_t launch_gemm_f16(const TcGemm& tg, const CUtensorMap& tmBhi16, const CUtensorMap& tmBlo16, float* Mo,
                             int P, int64_t t_lo, int64_t T, int64_t T_s, int C, int K, const unsigned int* vmax,
-                            const float* uscal, cudaStream_t s, int zmask = 0, bool vres = true);
+                            const float* uscal, cudaStream_t s, int zmask = 0, bool vres = true,
+                            const DFoldGemm* df = nullptr);
 // U (fp32) -> scaled fp16 hi / lo halves; *uscal = 2^su (mx: scratch word)
 cudaError_t launch_split16(const float* u32, int64_t n, unsigned int* mx, void* hi, void* lo, float* uscal,
                            cudaStream_t s);
@@ -123,7 +136,15 @@ constexpr int kMaxUFoldQ = 64, kMaxUFoldMO = 8;
 struct UFoldTab {
   double coef[kMaxUFoldQ][kMaxUFoldMO];   // exact product of A^T entries, RNE to fp64
   int Q, MO;
+  // direct-axis fold (F = 1, xform_dfold.cu): row (q, c) is tap j = q of the
+  // raw last axis, U'[xo][(j,c)][(o,k)] = (g x_outer G)[xo][c][k][j - o]
+  // (coef[j][o] = 1 for 0 <= j - o < r, else 0): the last axis takes the
+  // filter tap itself instead of G
+  int direct;
 };
+// a2 of the direct-axis fold: x -> Z [P/alpha * 2][C][Tz] by launch_input_xform
+// with g.dfold set (xform_in.cuh); the shapes it takes (xform_dfold.cu)
+bool input_dfold_supported(int N, int alpha, int m, int spec, int tiles_last);
 // U' [P/Q][Q*C][K_s'] (K_s' >= MO*K, = fp.K_s) from g; fp.P / fp.C / fp.K are the layer's
 cudaError_t launch_filter_ufold(const float* g, float* Uhi, float* Ulo, float* U32, const FParams& fp,
                                 const UFoldTab& uf, cudaStream_t s);

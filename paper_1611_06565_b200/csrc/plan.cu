@@ -233,6 +233,13 @@ struct wino_plan_s {
   int64_t gP = 0;
   int gC = 0, gK = 0;
   int zmask = 0;   // U' chunks that are zero by construction (skipped by the V-resident f16 GEMM)
+  // a5 direct-axis fold (xform_dfold.cu, reading #21): with uf_F = 1,
+  // B^T of the last axis is folded into U' as well -- the GEMM's A operand is
+  // Z (outer axes transformed, last axis raw; in the V buffer), U' holds the
+  // outer-axes filter transform per tap, and the last axis is computed directly
+  bool df = false;
+  int64_t df_Tz = 0;          // slot pitch of a Z plane
+  CUtensorMap tmA_df{};
   bool f16n = true;   // 3xFP16: the V-resident kernel where it applies (WINO_F16N=0, dev knob: k_gemm_f16p)
   // 3xFP16 GEMM (gemm_f16.cu): U as scaled fp16 halves in ubuf (hi | lo |
   // tail: uscal, umax | fp32 staging of the filter transform), vmax: max|V|
@@ -365,6 +372,18 @@ static void fold_coefs(const Transforms& t, int F, UFoldTab& uf) {
       }
       uf.coef[q][o] = rat_to_f64(c);
     }
+}
+
+// a5 direct-axis fold on top of the filter-side fold F = 1 where it applies
+// (F(2^3,3^3), V-resident 3xFP16 GEMM): default on (measured);
+// WINO_DFOLD=0 (dev knob) keeps the plain filter-side fold.
+// Default rule: at least 24 tiles along the last axis (Z rows are 32 slots
+// wide, so fewer tiles waste GEMM rows); WINO_DFOLD=1 takes it wherever the
+// kernels apply (tests), 0 never.
+static bool dfold_wanted(int tiles_last) {
+  const char* ev = getenv("WINO_DFOLD");
+  if (ev) return atoi(ev) != 0;
+  return tiles_last >= 24;
 }
 
 // Zero U' chunks of the filter-side fold: bit nb * 8 + ch is set when every
@@ -564,7 +583,18 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
   const size_t ucount = (size_t)p->gP * p->gC * p->K_s;   // U, or U' under the filter-side fold
   const int nbuf = p->gemm_mode == WINO_GEMM_FFMA ? 1 : 2;
   p->filter_bytes = ucount * 4 * nbuf + (p->f16 ? 256 : 0);
-  p->ws_bytes = ((size_t)p->P * C * p->T_s + (size_t)p->P * K * p->T_s) * 4;
+  // a5 direct-axis fold candidate (decided below, once the GEMM's k-chunk is
+  // known): Z [gP * 2][C][df_Tz] shares the V region, which is sized for both
+  const bool df_cand = p->uf_F == 1 && r == 3 && !p->chunked && p->gemm_mode == WINO_GEMM_3XF16 &&
+                       !mixed && g.nbox1 == 1 && input_dfold_supported(N, a, m, spec, p->tiles[N - 1]) &&
+                       dfold_wanted(p->tiles[N - 1]);
+  size_t v_floats = (size_t)p->P * C * p->T_s;
+  if (df_cand) {
+    p->df_Tz = ((int64_t)batch * p->tiles[0] * p->tiles[1] * 32 + 255) / 256 * 256;
+    const size_t z_floats = (size_t)p->gP * 2 * C * p->df_Tz;
+    if (z_floats > v_floats) v_floats = z_floats;
+  }
+  p->ws_bytes = (v_floats + (size_t)p->P * K * p->T_s) * 4;
   cudaError_t e = cudaMalloc(&p->ubuf, p->filter_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&p->V, p->ws_bytes);
   if (e == cudaSuccess && p->f16) e = cudaMalloc(&p->vmax, 256);
@@ -577,7 +607,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
     return fail(e == cudaErrorMemoryAllocation ? WINO_ERR_NOMEM : WINO_ERR_CUDA, "device allocation failed: %s",
                 cudaGetErrorString(e));
   }
-  p->M = p->V + (size_t)p->P * C * p->T_s;
+  p->M = p->V + v_floats;
   // GEMM padding rows t in [T, T_s) of V are never written: zero them once
   e = zero_private(p->V, p->ws_bytes);
   if (e != cudaSuccess) {
@@ -624,6 +654,15 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
       e = f16_encode_u(&p->tmBhi16, p->U16hi, p->K_s, gC, gP, p->tg.kc);
       if (e == cudaSuccess) e = f16_encode_u(&p->tmBlo16, p->U16lo, p->K_s, gC, gP, p->tg.kc);
       if (const char* ev = getenv("WINO_F16N")) p->f16n = atoi(ev) != 0;
+      if (df_cand && p->f16n && C % p->tg.kc == 0 && f16n_applies(gC, gK, p->tg.kc)) {
+        // direct-axis fold: Z planes of 32-slot rows in the V buffer
+        if (f16_encode_z(&p->tmA_df, p->V, p->df_Tz, C, (int)p->gP * 2, p->tg.kc) == cudaSuccess) {
+          p->df = true;
+          p->uf_tab.direct = 1;
+          for (int j = 0; j < a; ++j)
+            for (int o = 0; o < m; ++o) p->uf_tab.coef[j][o] = (j - o >= 0 && j - o < r) ? 1.0 : 0.0;
+        }
+      }
       if (p->uf_F && p->f16n && C % p->tg.kc == 0 && f16n_applies(gC, gK, p->tg.kc)) p->zmask = ufold_zmask(p, 128);
     }
     if (e == cudaSuccess && !p->uf_F && !mixed && !p->chunked && p->gemm_mode == WINO_GEMM_3XTF32) plan_fold(p);
@@ -931,6 +970,8 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     const int64_t s1 = s0 + step < nslab ? s0 + step : nslab;
     const int64_t t_lo = slab_tile(g, s0), t_hi = slab_tile(g, s1);
     g.s_beg = s0;
+    g.dfold = p->df ? 1 : 0;   // a2 writes Z (outer axes only) into the V region
+    g.Tz = p->df_Tz;
     g.t0 = p->chunked ? t_lo : 0;
     g.t_beg = t_lo;
     g.T = t_hi;
@@ -946,7 +987,13 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     ProfScope pg{p, s, 1};
     if (rec) CUDA_TRY(pg.begin());
     pdl_stage(2);
-    if (p->f16) {
+    if (p->df) {
+      // the GEMM's rows are Z's slots: 32 per (b, t_0, t_1) row of tiles
+      const DFoldGemm dg{&p->tmA_df, p->tiles[p->N - 1], p->C};
+      const int64_t slots = (int64_t)B * p->tiles[0] * p->tiles[1] * 32;
+      CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->gP, 0, slots, p->T_s, p->gC, p->gK,
+                               p->vmax, p->uscal, s, p->zmask, true, &dg));
+    } else if (p->f16) {
       CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->gP, t_lo - g.t0, t_hi - g.t0, p->T_s,
                                p->gC, p->gK, p->vmax, p->uscal, s, p->zmask, p->f16n));
     } else if (p->fold_F) {
@@ -1068,7 +1115,7 @@ wino_status wino_plan_info(wino_plan_t p, int64_t* info) {
                          p->gemm_mode == WINO_GEMM_FFMA ? -1 : p->tg.variant, p->geom.bt0,
                          p->geom.npl, p->nd ? 2 : p->mixed ? 1 : 0, p->tiny ? 1 : 0, launches,
                          p->nd ? 0 : p->geom.nbox1, p->fold_F + p->uf_F,
-                         p->uf_F ? 2 : p->fold_F ? 1 : 0};
+                         p->df ? 3 : p->uf_F ? 2 : p->fold_F ? 1 : 0};
   memcpy(info, v, sizeof v);
   return WINO_OK;
 }

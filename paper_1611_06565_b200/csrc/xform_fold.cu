@@ -62,6 +62,8 @@ k_output_fold(const float* __restrict__ W, float* __restrict__ y, const __grid_c
   constexpr int MN = ipow(M, N);
   pdl_wait();      // W comes from the folded GEMM
   pdl_trigger();
+  // the GEMM has consumed max|V| (3xFP16 scaling): clear it for the next forward
+  if (g.vmax_reset && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *g.vmax_reset = 0u;
   const int64_t t = g.t_beg + (int64_t)blockIdx.x * 128 + threadIdx.x;
   const int k = blockIdx.y;
   if (t >= g.T) return;

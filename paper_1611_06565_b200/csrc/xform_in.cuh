@@ -399,6 +399,54 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     return V + (int64_t)pl[p].c * g.T_s +
            ((int64_t)pl[p].b * g.Tps + (int64_t)pl[p].a0 * g.R + (int64_t)pl[p].a1 * g.R1 - g.t0);
   };
+  // ---- a5 direct-axis fold (xform_dfold.cu): the outer axes 0 and 1 only.
+  // One warp item per (plane, t_0, t_1): lane i owns the slab-column pair
+  // (2i, 2i+1) of the zero-padded row (i <= tiles_2), transforms its two
+  // alpha x alpha (i_0, i_1) windows and writes one 128-byte line of slots
+  // row * 32 + i per (xo, parity) plane of Z; the warps of a block hold
+  // consecutive t_1, i.e. consecutive lines.
+  if constexpr (N == 3 && A == 4 && M == 2 && Ax::A == 4 && Ax::M == 2) {
+    if (g.dfold) {
+      using Get = BTget<Tab>;
+      const int tl1 = g.tiles[1], tl2 = g.tiles[2];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+      const int64_t zstride = (int64_t)g.C * g.Tz;
+      const int per = g.bt0 * tl1;               // warp items of a full-depth slab
+      const int sst0 = g.sst[0], sst1 = g.sst[1];
+      for (int u = warp; u < npl * per; u += nwarps) {
+        const int p = u / per, w = u - p * per;
+        const int t0l = w / tl1, t1 = w - t0l * tl1;
+        if (t0l >= pl[p].nt0) continue;
+        ensure(p);
+        // every lane stores: the padding slots (lane > tiles_2) get zeros, so each
+        // warp store is one full 128-byte line (29-lane stores left partial
+        // sectors that L2 completed with DRAM reads: +0.23 GB read on c3)
+        const bool act = lane <= tl2;
+        const float* sp = S0 + p * slab_f + t0l * M * sst0 + t1 * M * sst1 + (act ? 2 * lane : 0) + D;
+        float he[A * A], ho[A * A];
+#pragma unroll
+        for (int i0 = 0; i0 < A; ++i0) {
+#pragma unroll
+          for (int i1 = 0; i1 < A; ++i1) {
+            he[i0 * A + i1] = act ? sp[i0 * sst0 + i1 * sst1] : 0.f;
+            ho[i0 * A + i1] = act ? sp[i0 * sst0 + i1 * sst1 + 1] : 0.f;
+          }
+        }
+        all_axes<A, 2, A, A, Get>(he, xp);
+        all_axes<A, 2, A, A, Get>(ho, xp);
+        float* zp = V + (int64_t)pl[p].c * g.Tz +
+                    (((int64_t)pl[p].b * g.tiles[0] + pl[p].a0 + t0l) * tl1 + t1) * 32 + lane;
+#pragma unroll
+        for (int q = 0; q < A * A; ++q) {
+          vput(zp + (2 * q) * zstride, he[q], vm);
+          vput(zp + (2 * q + 1) * zstride, ho[q], vm);
+        }
+        vtrack<A * A>(g, he, vm);
+        vtrack<A * A>(g, ho, vm);
+      }
+      return;
+    }
+  }
   // ---- N = 3, alpha >= 6: the axis-0 pass materialised in shared memory
   if constexpr (N == 3 && A >= 6) {
     using Get = BTget<Tab>;

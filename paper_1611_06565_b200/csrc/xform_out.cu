@@ -162,7 +162,12 @@ k_filter_ufold(const float* __restrict__ g, float* __restrict__ Uhi, float* __re
     for (int p = 0; p < rN; ++p) {
       double w = 1.0;
       int pq = p;
-      for (int n = fp.N - 1; n >= 0; --n) { w *= fp.G[n][xd[n]][pq % fp.r[n]]; pq /= fp.r[n]; }
+      for (int n = fp.N - 1; n >= 0; --n) {
+        // direct-axis fold: the last axis keeps the raw tap j - o (q = j)
+        if (uf.direct && n == fp.N - 1) w *= (pq % fp.r[n] == q - o) ? 1.0 : 0.0;
+        else w *= fp.G[n][xd[n]][pq % fp.r[n]];
+        pq /= fp.r[n];
+      }
       if (w != 0.0) acc = fma(w, (double)__ldg(gk + p), acc);
     }
     u = (float)(cf * acc);

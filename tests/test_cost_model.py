@@ -173,6 +173,14 @@ def test_stage_model_fold_bytes():
     assert s1["gemm"]["bytes"] == Vb + 2 * Ub + Mb // 2
     assert s1["gemm"]["flops"] == 2 * s0["gemm"]["flops"]
     assert s1["output_xform"]["bytes"] == s0["output_xform"]["bytes"] - Mb // 2
+    # direct-axis fold (fold_mode 3): Z = 16 outer points x 58 padded columns per
+    # row of 28 tiles instead of V = 64 points x 28 tiles; 2 * 3 / 4 of the flops
+    s3 = stage_model(*args, fold=1, fold_mode=3)
+    Zb = 4 * 16 * C * (T // 28) * 58
+    assert s3["input_xform"]["bytes"] == s0["input_xform"]["bytes"] - Vb + Zb
+    assert s3["gemm"]["bytes"] == Zb + 2 * Ub + Mb // 2
+    assert 2 * s3["gemm"]["flops"] == 3 * s0["gemm"]["flops"]
+    assert s3["output_xform"] == s1["output_xform"]
     s2 = stage_model(*args, fold=2, fold_mode=1)
     assert s2["gemm"]["bytes"] == Vb + Ub + Mb // 4 and s2["gemm"]["flops"] == s0["gemm"]["flops"]
     assert s2["input_xform"] == s0["input_xform"]

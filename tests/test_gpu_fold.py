@@ -132,7 +132,9 @@ def test_fold_off_where_infeasible_or_slower(monkeypatch):
     # counts (k-chunk < 32) or chunked plans
     monkeypatch.delenv("WINO_FOLD", raising=False)
     monkeypatch.delenv("WINO_UFOLD", raising=False)
-    for name, want in (("c3", (1, 2)), ("c5", (2, 1)), ("c2", (0, 0)), ("c4", (0, 0))):
+    monkeypatch.delenv("WINO_DFOLD", raising=False)
+    # (c3: the filter-side fold with the direct-axis fold on top, fold_mode 3, tests/test_gpu_dfold.py)
+    for name, want in (("c3", (1, 3)), ("c5", (2, 1)), ("c2", (0, 0)), ("c4", (0, 0))):
         cfg = CONFIGS[name]
         plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, 2, cfg.padding)
         assert (plan.info["fold"], plan.info["fold_mode"]) == want, (name, plan.info)

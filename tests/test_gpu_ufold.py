@@ -37,6 +37,7 @@ def _cuda():
 
 def _plan(cfg, F, scheme, monkeypatch, batch):
     monkeypatch.setenv("WINO_UFOLD", str(F))
+    monkeypatch.setenv("WINO_DFOLD", "0")   # the plain filter-side fold (the direct-axis fold: test_gpu_dfold.py)
     monkeypatch.setenv("WINO_FOLD", "0")
     monkeypatch.setenv("WINO_GEMM_AUTO_MODE", SCHEMES[scheme])
     return pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, batch, cfg.padding)
@@ -154,9 +155,10 @@ def test_ufold_default(monkeypatch):
     # default plans (no knobs): F(2^3, 3^3) takes the filter-side fold F = 1
     # on the 3xFP16 GEMM (measured fastest on c3); N = 4 keeps the epilogue
     # fold, F(4^N, 3^N) no fold
-    for k in ("WINO_UFOLD", "WINO_FOLD", "WINO_GEMM_AUTO_MODE"):
+    for k in ("WINO_UFOLD", "WINO_FOLD", "WINO_GEMM_AUTO_MODE", "WINO_DFOLD"):
         monkeypatch.delenv(k, raising=False)
-    want = {"c3": (1, 2, 4), "c5": (2, 1, 3), "c2": (0, 0, 4), "c4": (0, 0, 4)}
+    # (c3: fold_mode 3 = the filter-side fold with the direct-axis fold on top)
+    want = {"c3": (1, 3, 4), "c5": (2, 1, 3), "c2": (0, 0, 4), "c4": (0, 0, 4)}
     for name, (F, mode, gm) in want.items():
         cfg = CONFIGS[name]
         plan = pkg.Plan(cfg.N, cfg.dims, cfg.m, cfg.r, cfg.C, cfg.K, 2, cfg.padding)
