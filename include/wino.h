@@ -196,7 +196,13 @@ WINO_API wino_status wino_plan_sizes(wino_plan_t plan, size_t* workspace_bytes, 
  * of the accumulators, gemm_fold.cu; 2: filter-side fold, A^T of those axes
  * multiplied into the cached transformed filter U' at wino_filter_transform
  * time and the GEMM run as (n_points / alpha^F) GEMMs of depth alpha^F * C
- * and width m^F * K; 0: none). */
+ * and width m^F * K; 3: the direct-axis fold, F = 1 -- as 2, and B^T of the
+ * innermost axis is folded into U' as well, so the input transform covers
+ * the outer axes only (the workspace's V region then holds Z [n_points /
+ * alpha * 2][C][slots], 32 slots per row of tiles of the last axis: even /
+ * odd zero-padded input columns) and the GEMM computes the innermost axis as
+ * a direct correlation, PAPER.md:52-56 / Eq. (4); same results within the
+ * plan's tolerance; 0: none). */
 WINO_API wino_status wino_plan_info(wino_plan_t plan, int64_t* info);
 
 /* ---- multi-GPU hooks (U is computed once and NCCL-broadcast) ------------------
@@ -207,7 +213,10 @@ WINO_API wino_status wino_filter_mark_ready(wino_plan_t plan);
 
 /* ---- test / stage hooks --------------------------------------------------------
  * Device pointers of the unfused workspace: V [n_points][C][T_stride] and
- * M [n_points][K][T_stride] (valid after a forward with fuse == 0). */
+ * M [n_points][K][T_stride] (valid after a forward with fuse == 0).  Under
+ * an a5 fold (wino_plan_info fold_mode) the M region holds W
+ * [n_points / alpha^F * m^F][K][T_stride]; under fold_mode 3 the V region
+ * holds Z (see wino_plan_info). */
 WINO_API wino_status wino_workspace(wino_plan_t plan, void** V, void** M);
 
 /* Per-stage CUDA-event timing of forward calls (bench instrumentation).

@@ -101,6 +101,8 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   }
   g.in_flags = 0;
   if (const char* ev = getenv("WINO_IN_FLAGS")) g.in_flags = atoi(ev);  // dev A/B knob
+  g.in_prefetch = 0;
+  if (const char* ev = getenv("WINO_IN_PREFETCH")) g.in_prefetch = atoi(ev);
   g.in_pad8 = 0;
   g.slab_bytes = (int)slab(bt0);
   g.slot_bytes = (g.slab_bytes + 127) / 128 * 128;

@@ -347,6 +347,25 @@ __device__ __forceinline__ void load_slab_cpasync(float* S, const float* __restr
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
+// L2 prefetch of the box issue_slab_tma would load (no shared-memory destination, no barrier).
+template <int N, int M, int D>
+__device__ __forceinline__ void prefetch_slab_tma(const CUtensorMap* tm, const KGeom& g, int b, int a0, int c, int o1) {
+  int co[5];
+  co[0] = -g.pad[N - 1] - D;
+#pragma unroll
+  for (int ax = 0; ax < N - 1; ++ax) co[N - 1 - ax] = (ax == 0 ? a0 * M : ax == 1 ? o1 : 0) - g.pad[ax];
+  co[N] = b * g.C + c;
+  if constexpr (N == 2)
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tm), "r"(co[0]), "r"(co[1]),
+                 "r"(co[2]) : "memory");
+  else if constexpr (N == 3)
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(tm), "r"(co[0]),
+                 "r"(co[1]), "r"(co[2]), "r"(co[3]) : "memory");
+  else
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(tm), "r"(co[0]),
+                 "r"(co[1]), "r"(co[2]), "r"(co[3]), "r"(co[4]) : "memory");
+}
+
 // Issue the TMA box of plane (b, box, c) into slab S (thread 0 only).
 template <int N, int M, int D>
 __device__ __forceinline__ void issue_slab_tma(float* S, const CUtensorMap* tm, const KGeom& g, int b, int a0, int c,
@@ -806,6 +825,15 @@ k_input_xform(const float* __restrict__ x, float* __restrict__ V, const __grid_c
     if (threadIdx.x < npl) {
       const int p = threadIdx.x;
       issue_slab_tma<N, Ax::M, D>(smem_f + p * slab_f, &tm, g, mine.b, mine.a0, mine.c, mine.a1 * M, mb0 + 8u * p);
+    }
+    // the slabs of the CTA that will follow this one on its SM: under the
+    // layer's write traffic a DRAM read takes microseconds, an L2 hit does not
+    if (g.in_prefetch > 0 && threadIdx.x < g.npl) {
+      const long long wn = (long long)w0 + (long long)g.in_prefetch * g.npl + threadIdx.x;
+      if (wn < nwork) {
+        const PlaneInfo q = plane((int)wn);
+        prefetch_slab_tma<N, Ax::M, D>(&tm, g, q.b, q.a0, q.c, q.a1 * M);
+      }
     }
     __syncthreads();
   } else {
