@@ -85,6 +85,7 @@ struct KGeom {
   // a5 direct-axis fold (xform_dfold.cu): a2 transforms the outer axes only and
   // writes Z [P/alpha * 2][C][Tz] (32-slot rows) instead of V
   int dfold;
+  int df_S;                    // slots per row of tiles (32; > tiles_last)
   int64_t Tz;                  // slot pitch of a Z plane
 };
 

@@ -330,18 +330,18 @@ k_gemm_f16p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // U chunk (nb, c) is zero by construction (filter-side fold, A^T_F[o][q] = 0
 // for every column of the n-block), its U load and MMAs are skipped.
 // DF (direct-axis fold, xform_dfold.cu): the A operand is Z [P*2][df_cz][Tz]
-// in 32-slot rows; k-chunk ch holds tap j = ch*KC / df_cz (df_cz a multiple of
+// in rows of df_S slots; k-chunk ch holds tap j = ch*KC / df_cz (df_cz a multiple of
 // KC), loaded as the {BM + 4, KC} box of plane xi*2 + (j & 1) at the unit's
 // 16-byte aligned first slot (TMA start coordinates must be 16-byte aligned:
 // tools/tma_off_probe.cu) and read by the converter at slot + (j >> 1); T
-// counts slots, and the epilogue stores slot (row, i < df_tl2) at tile
-// row * df_tl2 + i of W (a warp's 32 TMEM lanes are one row).
+// counts slots (df_S per row of tiles), and the epilogue stores
+// slot (row, i < df_tl2) at tile row * df_tl2 + i of W.
 template <int BN, int KC, int NB, bool DF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsTS, 1)
 k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
             const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ Mo, int P, int t_lo, int T, long long T_s,
             int C, int K, int nraw, int nbr, int l2hint, const unsigned int* __restrict__ vmax,
-            const float* __restrict__ uscal, int zmask, int df_tl2, int df_cz) {
+            const float* __restrict__ uscal, int zmask, int df_tl2, int df_cz, int df_S) {
   constexpr int BMR = DF ? BM + 4 : BM;   // raw-stage row pitch (slots)
   constexpr int HN = BN / 2;
   static_assert(HN == 64, "one 64-wide fp16 swizzle group per CTA half");
@@ -572,9 +572,10 @@ k_gemm_f16n(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const int mp = (int)(u % n_mp);
       int t = t_lo + mp * 2 * BM + (int)rank * BM + q * 32 + lane;
       bool live = t < T;
-      if constexpr (DF) {   // slot (row, lane) -> tile row * tl2 + lane; slots >= tl2 of a row are padding
-        live = live && lane < df_tl2;
-        t = (t >> 5) * df_tl2 + lane;
+      if constexpr (DF) {   // slot row * S + i -> tile row * tl2 + i; slot i = tl2 of a row only feeds the taps
+        const int zr = t / df_S, zi = t - zr * df_S;
+        live = live && zi < df_tl2;
+        t = zr * df_tl2 + zi;
       }
       for (int nb = 0; nb < NB; ++nb) {
         mbar_wait(tfull(nb), uphase);
@@ -748,7 +749,7 @@ static cudaError_t launch_f16n_kc(const TcGemm& tg, const CUtensorMap& tmBhi16, 
   const long long Ts = T_s;
   return launch_pdl(kern, dim3((unsigned)(2 * pairs)), dim3(tc::kThreadsTS), smem, s, DF ? *df->tmA : tg.tmA_ts, tmBhi16,
                     tmBlo16, Mo, P, (int)t_lo, (int)T, Ts, C, K, nraw, nbr, l2hint, vmax, uscal, zmask, DF ? df->tl2 : 0,
-                    DF ? df->cz : 0);
+                    DF ? df->cz : 0, DF ? df->S : 1);
 }
 
 // Z of the direct-axis fold as (slot, c, plane): box {BM + 4, kc, 1}, no swizzle, zero fill past Tz

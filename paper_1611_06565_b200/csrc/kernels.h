@@ -92,11 +92,13 @@ bool f16n_applies(int C, int K, int kc);
 // is Z [P*2][cz][Tz] -- k-chunk (tap j, channels c0..) of unit (xo, 256-slot
 // block) is the box of plane xo*2 + (j & 1) at slot + (j >> 1) (loaded from
 // the 16-byte aligned slot, the shift applied by the converter); T counts
-// slots (rows * 32) and the epilogue stores slot (row, i < tl2) at tile
+// slots (rows * S) and the epilogue stores slot (row, i < tl2) at tile
 // row * tl2 + i of W.
+constexpr int kDfoldSlots = 32;   // full 128-byte lines per row (packed rows of tl2 + 1 slots measured slower)
 struct DFoldGemm {
   const CUtensorMap* tmA;   // Z as (slot, c, plane), box {132, kc, 1}, no swizzle (f16_encode_z)
   int tl2;                  // tiles along the last axis (<= 31)
+  int S;                    // slots per row of tiles (kDfoldSlots)
   int cz;                   // layer channels C (a multiple of the k-chunk)
 };
 cudaError_t f16_encode_z(CUtensorMap* tm, const float* Z, int64_t Tz, int cz, int planes, int kc);

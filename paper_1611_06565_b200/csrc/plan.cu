@@ -378,8 +378,8 @@ static void fold_coefs(const Transforms& t, int F, UFoldTab& uf) {
 // (F(2^3,3^3), V-resident 3xFP16 GEMM): default on (measured);
 // WINO_DFOLD=0 (dev knob) keeps the plain filter-side fold.
 // Default rule: at least 24 tiles along the last axis (Z rows are 32 slots
-// wide, so fewer tiles waste GEMM rows); WINO_DFOLD=1 takes it wherever the
-// kernels apply (tests), 0 never.
+// wide, so fewer tiles waste GEMM rows);
+// WINO_DFOLD=1 takes it wherever the kernels apply (tests), 0 never.
 static bool dfold_wanted(int tiles_last) {
   const char* ev = getenv("WINO_DFOLD");
   if (ev) return atoi(ev) != 0;
@@ -590,7 +590,7 @@ static wino_status create_core(wino_plan_t* plan_out, int N, const int64_t* dims
                        dfold_wanted(p->tiles[N - 1]);
   size_t v_floats = (size_t)p->P * C * p->T_s;
   if (df_cand) {
-    p->df_Tz = ((int64_t)batch * p->tiles[0] * p->tiles[1] * 32 + 255) / 256 * 256;
+    p->df_Tz = ((int64_t)batch * p->tiles[0] * p->tiles[1] * kDfoldSlots + 255) / 256 * 256;
     const size_t z_floats = (size_t)p->gP * 2 * C * p->df_Tz;
     if (z_floats > v_floats) v_floats = z_floats;
   }
@@ -972,6 +972,7 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     g.s_beg = s0;
     g.dfold = p->df ? 1 : 0;   // a2 writes Z (outer axes only) into the V region
     g.Tz = p->df_Tz;
+    g.df_S = kDfoldSlots;
     g.t0 = p->chunked ? t_lo : 0;
     g.t_beg = t_lo;
     g.T = t_hi;
@@ -989,8 +990,8 @@ static wino_status forward_impl(wino_plan_t p, const float* x, float* y, int B, 
     pdl_stage(2);
     if (p->df) {
       // the GEMM's rows are Z's slots: 32 per (b, t_0, t_1) row of tiles
-      const DFoldGemm dg{&p->tmA_df, p->tiles[p->N - 1], p->C};
-      const int64_t slots = (int64_t)B * p->tiles[0] * p->tiles[1] * 32;
+      const DFoldGemm dg{&p->tmA_df, p->tiles[p->N - 1], kDfoldSlots, p->C};
+      const int64_t slots = (int64_t)B * p->tiles[0] * p->tiles[1] * kDfoldSlots;
       CUDA_TRY(launch_gemm_f16(p->tg, p->tmBhi16, p->tmBlo16, p->M, (int)p->gP, 0, slots, p->T_s, p->gC, p->gK,
                                p->vmax, p->uscal, s, p->zmask, true, &dg));
     } else if (p->f16) {

@@ -421,9 +421,15 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
   // ---- a5 direct-axis fold (xform_dfold.cu): the outer axes 0 and 1 only.
   // One warp item per (plane, t_0, t_1): lane i owns the slab-column pair
   // (2i, 2i+1) of the zero-padded row (i <= tiles_2), transforms its two
-  // alpha x alpha (i_0, i_1) windows and writes one 128-byte line of slots
-  // row * 32 + i per (xo, parity) plane of Z; the warps of a block hold
-  // consecutive t_1, i.e. consecutive lines.
+  // alpha x alpha (i_0, i_1) windows and writes the S = g.df_S slots row * S
+  // + i of its row per (xo, parity) plane of Z (slots past tiles_2 get zeros);
+  // the warps of a block hold consecutive t_1, i.e. one contiguous run of
+  // slots per plane.  S = 32: every warp store is one full 128-byte line.
+  // Measured on c3: storing only the 29 data lanes of a 32-slot row left a
+  // partial sector in every line, which L2 completed from DRAM (+0.23 GB
+  // read, 0.46 instead of 0.20 ms); rows packed at S = 29 (116-byte stores
+  // whose sectors complete in L2, 9% fewer GEMM rows) took 0.245 ms and the
+  // GEMM 0.53 instead of 0.505 ms.
   if constexpr (N == 3 && A == 4 && M == 2 && Ax::A == 4 && Ax::M == 2) {
     if (g.dfold) {
       using Get = BTget<Tab>;
@@ -437,9 +443,6 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         const int t0l = w / tl1, t1 = w - t0l * tl1;
         if (t0l >= pl[p].nt0) continue;
         ensure(p);
-        // every lane stores: the padding slots (lane > tiles_2) get zeros, so each
-        // warp store is one full 128-byte line (29-lane stores left partial
-        // sectors that L2 completed with DRAM reads: +0.23 GB read on c3)
         const bool act = lane <= tl2;
         const float* sp = S0 + p * slab_f + t0l * M * sst0 + t1 * M * sst1 + (act ? 2 * lane : 0) + D;
         float he[A * A], ho[A * A];
@@ -454,11 +457,13 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
         all_axes<A, 2, A, A, Get>(he, xp);
         all_axes<A, 2, A, A, Get>(ho, xp);
         float* zp = V + (int64_t)pl[p].c * g.Tz +
-                    (((int64_t)pl[p].b * g.tiles[0] + pl[p].a0 + t0l) * tl1 + t1) * 32 + lane;
+                    (((int64_t)pl[p].b * g.tiles[0] + pl[p].a0 + t0l) * tl1 + t1) * g.df_S + lane;
+        if (lane < g.df_S) {
 #pragma unroll
-        for (int q = 0; q < A * A; ++q) {
-          vput(zp + (2 * q) * zstride, he[q], vm);
-          vput(zp + (2 * q + 1) * zstride, ho[q], vm);
+          for (int q = 0; q < A * A; ++q) {
+            vput(zp + (2 * q) * zstride, he[q], vm);
+            vput(zp + (2 * q + 1) * zstride, ho[q], vm);
+          }
         }
         vtrack<A * A>(g, he, vm);
         vtrack<A * A>(g, ho, vm);

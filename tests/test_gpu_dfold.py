@@ -83,16 +83,20 @@ def test_dfold_stage_z_and_w(monkeypatch):
     win = np.stack([win0[:, :, :, :, i1:i1 + m * tiles[1]:m] for i1 in range(a)], 1)    # [i0][i1][b][c][t0][t1][col]
     Zref = np.einsum("xi,yj,ijbctuv->xycbtuv", Bt, Bt, win)
     rows = cfg.batch * tiles[0] * tiles[1]
-    Tz = (rows * 32 + 255) // 256 * 256
+    S = 32                                          # slots per row of tiles (kernels.h kDfoldSlots)
+    Tz = (rows * S + 255) // 256 * 256
     vptr, mptr = pkg.wino_workspace(plan.h)         # Z lives in the V region: [16 * 2][C][Tz]
     from paper_1611_06565_b200.wino import device_view
     Zg = device_view(vptr, (a * a * 2 * cfg.C * Tz,)).cpu().double().numpy().reshape(a, a, 2, cfg.C, Tz)
-    Zg = Zg[..., : rows * 32].reshape(a, a, 2, cfg.C, cfg.batch, tiles[0], tiles[1], 32)
+    tail = Zg[..., rows * S:]
+    Zg = Zg[..., : rows * S].reshape(a, a, 2, cfg.C, cfg.batch, tiles[0], tiles[1], S)
+    assert np.all(tail == 0)                        # the planes' tails stay zero
     for par in range(2):
         cols = Zref[..., par::2]                     # padded columns 2 i + par
-        got = Zg[:, :, par, ..., : cols.shape[-1]]
-        assert np.abs(got - cols).max() <= 4e-6 * np.abs(cols).max()
-        assert np.all(Zg[:, :, par, ..., cols.shape[-1]:] == 0)      # padding slots stay zero
+        nc = cols.shape[-1]
+        assert nc == tiles[2] + 1
+        assert np.abs(Zg[:, :, par, ..., :nc] - cols).max() <= 4e-6 * np.abs(cols).max()
+        assert np.all(Zg[:, :, par, ..., nc:] == 0)  # padding slots hold zeros
     # W as in tests/test_gpu_ufold.py
     _, st = wg.winograd_nd(xn, g.numpy().astype(np.float64), cfg.padding, A, B, C)
     T = cfg.tiles()
