@@ -73,6 +73,8 @@ struct KGeom {
   int in_threads;            // block size of the input kernel (<= 256; <= 512 in H mode)
   int smem_bytes;            // dynamic shared memory of the input kernel (npl slabs + H)
   int in_flags;              // dev A/B knob of the input kernel (WINO_IN_FLAGS; 0 in production)
+  int in_align;              // in-place H mode: phase-2 items laid out so that every warp stores one
+                             // 128-byte aligned line of V (WINO_IN_ALIGN)
   int in_prefetch;           // > 0: each CTA prefetches into L2 the slabs of the CTA in_prefetch blocks
                              // ahead (cp.async.bulk.prefetch.tensor), WINO_IN_PREFETCH
   int in_pad8;               // in-place H mode, m = 4: phase-2 items on 8 axis-2 slots per row

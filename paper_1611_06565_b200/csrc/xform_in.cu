@@ -101,6 +101,10 @@ bool plan_input_slab(KGeom& g, int N, int alpha0, int m0, int alpha, int m, bool
   }
   g.in_flags = 0;
   if (const char* ev = getenv("WINO_IN_FLAGS")) g.in_flags = atoi(ev);  // dev A/B knob
+  // line-aligned a2 work items: 1 = in-place H mode (c4 input 0.211 -> 0.185 ms), 2 = every path
+  // (dev A/B: slower on c2 / c3), 0 = off
+  g.in_align = 1;
+  if (const char* ev = getenv("WINO_IN_ALIGN")) g.in_align = atoi(ev);
   g.in_prefetch = 0;
   if (const char* ev = getenv("WINO_IN_PREFETCH")) g.in_prefetch = atoi(ev);
   g.in_pad8 = 0;

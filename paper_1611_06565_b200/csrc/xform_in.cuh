@@ -570,6 +570,37 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       // g.in_pad8: t2 runs over 8 slots per row (m = 4: window starts 16 bytes
       // apart, so the 8 lanes of a quarter warp read 8 distinct bank groups;
       // slots >= tl2 idle) -- no shared-memory bank conflicts
+      if (g.in_align) {
+        // line-aligned items: the CTA's planes are one contiguous run of t in
+        // every V plane; item v of a xi_0 group is tile v - lead of that run,
+        // lead = (run start) mod 32, so a warp's 32 lanes store one 128-byte
+        // aligned line (the run's first and last lines are shared with the
+        // neighbouring CTAs).  Planes of one channel only (same V row).
+        const int Rt = tl1 * tl2, ntile = npl * Rt;
+        const int lead = (int)((vbase(0) - V) & 31);
+        const int NR = (lead + ntile + 31) & ~31;
+        const bool onerow = pl[0].c == pl[npl - 1].c;
+        if (onerow) {
+          for (int u = threadIdx.x; u < A0 * NR; u += blockDim.x) {
+            const int xi0 = u / NR, tau = u - xi0 * NR - lead;
+            if (tau < 0 || tau >= ntile) continue;
+            const int p = tau / Rt, rem = tau - p * Rt;
+            const int t1 = rem / tl2, t2 = rem - t1 * tl2;
+            const float* hp0 = S0 + p * slab_f + xi0 * g.sst[0] + t1 * M * g.sst[1] + t2 * M;
+            float h[A * A];
+            if constexpr (A0 == 1) ensure(p);
+            constexpr int DS = A0 > 1 ? 0 : D;
+#pragma unroll
+            for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
+            all_axes<A, 2, A, A, Get>(h, xp);
+            float* vo = vbase(p) + rem + (int64_t)xi0 * (A * A) * pstride;
+#pragma unroll
+            for (int j = 0; j < A * A; ++j) vput(vo + j * pstride, h[j], vm);
+            vtrack<A * A>(g, h, vm);
+          }
+          return;
+        }
+      }
       const int tl2p = g.in_pad8 ? (tl2 + 7) / 8 * 8 : tl2;
       const int R = tl1 * tl2p, nrun = npl * R;
       // item u = ((xi0 * npl + p) * tl1 + t1) * tl2 + t2, stepped by the block
@@ -725,9 +756,15 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
       ensure(0);
       const int ntile = pl[0].nt0 * g.Rs;
       float* __restrict__ vb = vbase(0);
-      for (int w = threadIdx.x; w < NX * ntile; w += blockDim.x) {
-        const int xi0 = w / ntile;
-        const int tl = w - xi0 * ntile;
+      // g.in_align: item w of a xi_0 group is tile w - lead, lead = (the plane's
+      // first V row) mod 32, so a warp's lanes store one 128-byte aligned line
+      // (g.in_align >= 2 only: measured neutral on c5 and slower on c3's V path, 0.328 -> 0.335 ms)
+      const int lead = g.in_align >= 2 ? (int)((vb - V) & 31) : 0;
+      const int NR = g.in_align >= 2 ? ((lead + ntile + 31) & ~31) : ntile;
+      for (int w = threadIdx.x; w < NX * NR; w += blockDim.x) {
+        const int xi0 = w / NR;
+        const int tl = w - xi0 * NR - lead;
+        if (tl < 0 || tl >= ntile) continue;
         int rem = tl, base = 0;
 #pragma unroll
         for (int ax = N - 1; ax >= 1; --ax) {
@@ -744,12 +781,31 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
     }
     const int ntile = g.bt0 * g.Rs;           // tiles of a full-depth slab
     const int nper = NX * ntile;
-    for (int u = threadIdx.x; u < npl * nper; u += blockDim.x) {
-      const int p = u / nper;
-      const int w = u - p * nper;
-      const int xi0 = w / ntile;
-      const int tl = w - xi0 * ntile;
-      if (tl >= pl[p].nt0 * g.Rs) continue;   // last axis-0 box of a sample is shorter
+    // g.in_align, full-depth planes of one channel (one contiguous run of t in
+    // every V plane): pooled line-aligned items -- item v of a xi_0 group is
+    // tile v - lead of the run, lead = (run start) mod 32, so a warp's lanes
+    // store one 128-byte aligned line.  Otherwise items (plane, xi_0, tile).
+    // (g.in_align >= 2 only: measured slower on c2, input 33.1 -> 34.5 us)
+    const bool pooled = g.in_align >= 2 && pl[0].c == pl[npl - 1].c && pl[npl - 1].nt0 == g.bt0;
+    const int nrun = npl * ntile;
+    const int lead = pooled ? (int)((vbase(0) - V) & 31) : 0;
+    const int NR = (lead + nrun + 31) & ~31;
+    const int total = pooled ? NX * NR : npl * nper;
+    for (int u = threadIdx.x; u < total; u += blockDim.x) {
+      int p, xi0, tl;
+      if (pooled) {
+        xi0 = u / NR;
+        const int tau = u - xi0 * NR - lead;
+        if (tau < 0 || tau >= nrun) continue;
+        p = tau / ntile;
+        tl = tau - p * ntile;
+      } else {
+        p = u / nper;
+        const int w = u - p * nper;
+        xi0 = w / ntile;
+        tl = w - xi0 * ntile;
+        if (tl >= pl[p].nt0 * g.Rs) continue;   // last axis-0 box of a sample is shorter
+      }
       ensure(p);
       // local tile -> slab offset of its window
       int rem = tl, base = 0;

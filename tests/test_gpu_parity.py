@@ -275,6 +275,21 @@ def test_input_slabs_per_cta_bit_identical(name, monkeypatch):
         assert torch.equal(y0, y1), "npl=%s threads=%s (planned %d)" % (npl, thr, info1["in_planes_per_cta"])
 
 
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_input_line_aligned_items_bit_identical(name, monkeypatch):
+    # a2's line-aligned work items (default; item v of a run is tile v - lead,
+    # lead = run start mod 32, so every warp stores whole 128-byte lines of V)
+    # against the plain item order (WINO_IN_ALIGN=0), also with other slab
+    # groupings: only the item -> thread mapping changes, never the arithmetic
+    cfg = SMALL[name]
+    y0, _ = _run_env(cfg, monkeypatch, WINO_IN_ALIGN="0")
+    y1, _ = _run_env(cfg, monkeypatch, WINO_IN_ALIGN="2")     # 2: every a2 path (1, the default: in-place H mode)
+    assert torch.equal(y0, y1)
+    for npl, thr in (("1", "256"), ("3", "320"), ("4", "448")):
+        y2, _ = _run_env(cfg, monkeypatch, WINO_IN_ALIGN="2", WINO_IN_NPL=npl, WINO_IN_THREADS=thr)
+        assert torch.equal(y0, y2), "npl=%s threads=%s" % (npl, thr)
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_output_tma_ring_matches_plain(name, monkeypatch):
     # a4 reading M through the TMA ring (alpha^(N-1) >= 32) and through plain
