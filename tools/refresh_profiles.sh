@@ -9,7 +9,7 @@
 #   ${T}_reference.json   bench.py --impl reference (the oracle arm)
 #   ${T}_launches_c4.csv  ncu launch list (gpu__time_duration) of the headline bench command
 # usage: TAG=r02f bash tools/refresh_profiles.sh
-T=${TAG:-r02g}
+T=${TAG:-r02h}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/${T}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo smoke=$?
