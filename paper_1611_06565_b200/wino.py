@@ -14,6 +14,7 @@ WINO_ERR_CUDA through the ABI.
 from __future__ import annotations
 
 import ctypes
+import os
 import json
 from pathlib import Path
 from typing import Optional, Sequence
@@ -268,6 +269,10 @@ def device_view(ptr: int, shape, device=None):
     return torch.as_tensor(_CAI(ptr, shape), device=device or "cuda")
 
 
+def _nvtx_on() -> bool:
+    return os.environ.get("WINO_NVTX", "0") not in ("", "0")
+
+
 # ------------------------------------------------------------- Plan
 class Plan:
     """One N-D Winograd conv layer F(m^N, r^N) on one GPU.
@@ -336,10 +341,17 @@ class Plan:
         self._check_y(y, B)
         if bias is not None and tuple(bias.shape) != (self.K,):
             raise ValueError("bias has shape %s, the plan needs (%d,)" % (tuple(bias.shape), self.K))
-        if bias is None and not relu:
-            wino_forward(self.h, x, y, B, stream)
-        else:
-            wino_forward_ex(self.h, x, y, B, bias, WINO_ACT_RELU if relu else WINO_ACT_NONE, stream)
+        nvtx = _nvtx_on()
+        if nvtx:   # WINO_NVTX=1: an NVTX range around the ABI call (nsys / ncu --nvtx timelines)
+            torch.cuda.nvtx.range_push("wino_forward N=%d F(%s,%s) C=%d K=%d B=%d" % (self.N, self.m, self.r, self.C, self.K, B))
+        try:
+            if bias is None and not relu:
+                wino_forward(self.h, x, y, B, stream)
+            else:
+                wino_forward_ex(self.h, x, y, B, bias, WINO_ACT_RELU if relu else WINO_ACT_NONE, stream)
+        finally:
+            if nvtx:
+                torch.cuda.nvtx.range_pop()
         return y
 
     def forward_host(self, x_host, y_host, stream=None) -> None:

@@ -275,6 +275,14 @@ def test_input_slabs_per_cta_bit_identical(name, monkeypatch):
         assert torch.equal(y0, y1), "npl=%s threads=%s (planned %d)" % (npl, thr, info1["in_planes_per_cta"])
 
 
+def test_nvtx_range_around_forward(monkeypatch):
+    # WINO_NVTX=1: the binding wraps the ABI call in an NVTX range; same result
+    cfg = SMALL["c2"]
+    y0, _ = _run_env(cfg, monkeypatch)
+    y1, _ = _run_env(cfg, monkeypatch, WINO_NVTX="1")
+    assert torch.equal(y0, y1)
+
+
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
 def test_input_line_aligned_items_bit_identical(name, monkeypatch):
     # a2's line-aligned work items (default; item v of a run is tile v - lead,
