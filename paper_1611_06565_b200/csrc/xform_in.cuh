@@ -590,6 +590,7 @@ __device__ __forceinline__ void transform_planes(float* __restrict__ S0, int sla
             float h[A * A];
             if constexpr (A0 == 1) ensure(p);
             constexpr int DS = A0 > 1 ? 0 : D;
+            // (two 128-bit loads per row instead of 128 + 64 bits: no change, c4 input 0.185 ms either way)
 #pragma unroll
             for (int i1 = 0; i1 < A; ++i1) load_row<A, M, DS>(hp0 + i1 * g.sst[1], h + i1 * A);
             all_axes<A, 2, A, A, Get>(h, xp);
